@@ -1,0 +1,234 @@
+/*
+ * kvq_oracle.c — CPU ORACLE for per-channel symmetric INT8 KV-key quantization
+ * (arxiv 2601.04719). TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * `--impl reference` leg may load this file's library.  The product path
+ * (paper_2601_04719_b200/, libkvq.so) never links, includes or calls it, and
+ * this file includes nothing from the product.  The two share no code.
+ *
+ * Plain C99, single-threaded, no intrinsics.  Build flags (see oracle/__init__.py):
+ *   gcc -O2 -std=c99 -fno-fast-math -ffp-contract=off -shared -fPIC
+ * -ffp-contract=off keeps every product and sum separately rounded as written.
+ *
+ * Citations: P:<line> = /root/reference/PAPER.md line, S:<line> = SPEC.md line.
+ * Readings of silent/ambiguous passages are numbered Q1..Q16 as in SURVEY.md §8(c)
+ * and listed in DESIGN.md §3.
+ *
+ * Parity status of each function (what pins it, see tests/test_oracle_*.py):
+ *   kvqo_splitmix64 / kvqo_uniform   pinned: SURVEY §8(d) test vector + numpy re-implementation
+ *   kvqo_compute_scales              pinned: hand examples S:121-132, numpy abs-max, invariants
+ *   kvqo_absmax_rows                 pinned: equals kvqo_compute_scales on every shape tested
+ *   kvqo_quantize                    pinned: hand examples S:180-181, tie example, numpy rint,
+ *                                    brute force over all codes for fixed s
+ *   kvqo_dequantize                  pinned: S:189-191, numpy product
+ *   kvqo_recon_errors                pinned: identity, 3-4-5, closed form L2
+ *   kvqo_scores / kvqo_attention_abs_sum
+ *                                    pinned: [[1]] vs [[0.9]] -> 0.1, identity,
+ *                                    numpy float64 matmul, closed form sqrt(2/pi) s sqrt(D/36)
+ *   No function is "parity unpinned".
+ */
+#include <math.h>
+#include <stddef.h>
+#include <stdint.h>
+
+/* ------------------------------------------------------------------------ */
+/* Input generator; independent of the method's arithmetic.    */
+/* ------------------------------------------------------------------------ */
+
+/* splitmix64 keyed by (seed, global element index i), SURVEY §8(d). */
+uint64_t kvqo_splitmix64(uint64_t seed, uint64_t i)
+{
+    uint64_t z = seed + (i + 1u) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+/* Uniform on the exact lattice k * 2^-23, k in [-2^23, 2^23): "values in
+ * [-1, 1]", reading Q12. */
+float kvqo_uniform(uint64_t seed, uint64_t i)
+{
+    int32_t k = (int32_t)(kvqo_splitmix64(seed, i) >> 40) - (int32_t)(1 << 23);
+    return (float)k * 0x1p-23f; /* exact: |k| < 2^24 */
+}
+
+/* Fill rows [row0, row0+rows) of a T x D matrix (row-major, global index
+ * t*D + d), so a shard generated alone equals the same rows of the full matrix.
+ * dist 0: uniform lattice.
+ * dist 1: outlier channels: column d scaled by 2^(e_d), e_d = (splitmix64(seed ^
+ *         0xC0FFEE, d) mod 9) - 4 (motivates per-channel scales).
+ * dist 2: on-grid: x = c * s_d with s_d = j_d * 2^-24, j_d odd < 2^17, code c
+ *         uniform in [-127, 127] and row 0 forced to +-127.
+ */
+void kvqo_fill(float *out, int64_t row0, int64_t rows, int64_t D, uint64_t seed, int dist)
+{
+    for (int64_t r = 0; r < rows; r++) {
+        int64_t t = row0 + r;
+        for (int64_t d = 0; d < D; d++) {
+            uint64_t gi = (uint64_t)t * (uint64_t)D + (uint64_t)d;
+            float v;
+            if (dist == 1) {
+                int e = (int)(kvqo_splitmix64(seed ^ 0xC0FFEEull, (uint64_t)d) % 9u) - 4;
+                v = ldexpf(kvqo_uniform(seed, gi), e);
+            } else if (dist == 2) {
+                uint64_t j = ((kvqo_splitmix64(seed ^ 0x5CA1Eull, (uint64_t)d) >> 47) | 1u);
+                float s = (float)j * 0x1p-24f;
+                int c;
+                if (t == 0)
+                    c = (kvqo_splitmix64(seed ^ 0x516Eull, (uint64_t)d) & 1u) ? 127 : -127;
+                else
+                    c = (int)(kvqo_splitmix64(seed, gi) % 255u) - 127;
+                v = (float)c * s;
+            } else {
+                v = kvqo_uniform(seed, gi);
+            }
+            out[r * D + d] = v;
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* The method.                                                                */
+/* ------------------------------------------------------------------------ */
+
+/* Alg. 1 "Compute Scales" = Listing 2, Eq. 6:
+ *   for d: max_abs = 0; for t: if |K[t,d]| > max_abs then max_abs = |K[t,d]|;
+ *          scales[d] = max_abs / 127          (fp32 division, reading Q3)      */
+void kvqo_compute_scales(const float *K, int64_t T, int64_t D, float *scales)
+{
+    for (int64_t d = 0; d < D; d++) {
+        float max_abs = 0.0f;
+        for (int64_t t = 0; t < T; t++) {
+            float val = fabsf(K[t * D + d]);
+            if (val > max_abs)
+                max_abs = val;
+        }
+        scales[d] = max_abs / 127.0f;
+    }
+}
+
+/* The inner loop of Alg. 1 over a block of rows, carrying max_abs[d] across
+ * calls, so a matrix too large for host RAM can be streamed in row blocks.
+ * The max of Eq. 6 is over the set {|K[t,d]| : t}; it does not depend on the
+ * order in which t is visited, so visiting rows block by block computes the
+ * same max_abs as Alg. 1.  Caller zero-fills max_abs before the first block
+ * and finishes with kvqo_scales_from_absmax. */
+void kvqo_absmax_rows(const float *K, int64_t rows, int64_t D, float *max_abs)
+{
+    for (int64_t t = 0; t < rows; t++)
+        for (int64_t d = 0; d < D; d++) {
+            float val = fabsf(K[t * D + d]);
+            if (val > max_abs[d])
+                max_abs[d] = val;
+        }
+}
+
+/* Alg. 1 line "scales[d] <- max_abs / 127". */
+void kvqo_scales_from_absmax(const float *max_abs, int64_t D, float *scales)
+{
+    for (int64_t d = 0; d < D; d++)
+        scales[d] = max_abs[d] / 127.0f;
+}
+
+/* Eq. 7 = Listing 3:
+ *   q = round(K[t,d] / s_d), clamped to [-127, 127].
+ * Readings: Q1 round = round-half-even (rintf under FE_TONEAREST, as the GPU
+ * listings' __float2int_rn at P:272); Q2 the quotient is the fp32 IEEE quotient
+ * rounded to fp32 before rounding to an integer; Q4 symmetric clamp;
+ * Q5 s_d == 0 gives q = 0.  The clamp is applied to the rounded float before
+ * the int conversion (same result as Listing 3 for every finite quotient,
+ * and avoids converting out-of-range floats). */
+void kvqo_quantize(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq)
+{
+    for (int64_t t = 0; t < T; t++) {
+        for (int64_t d = 0; d < D; d++) {
+            float s = scales[d];
+            int q;
+            if (s == 0.0f) {
+                q = 0;
+            } else {
+                float val = K[t * D + d];
+                float v = val / s;
+                float r = rintf(v);
+                if (r > 127.0f)
+                    r = 127.0f;
+                if (r < -127.0f)
+                    r = -127.0f;
+                q = (int)r;
+            }
+            Kq[t * D + d] = (int8_t)q;
+        }
+    }
+}
+
+/* Eq. 8 = Listing 4: K_hat[t,d] = (float)q * s_d. */
+void kvqo_dequantize(const int8_t *Kq, const float *scales, int64_t T, int64_t D, float *K_hat)
+{
+    for (int64_t t = 0; t < T; t++)
+        for (int64_t d = 0; d < D; d++) {
+            int8_t q = Kq[t * D + d];
+            K_hat[t * D + d] = (float)q * scales[d];
+        }
+}
+
+/* Reconstruction errors (reading Q9):
+ *   sum_sq  += sum_i ((double)A_i - (double)B_i)^2   (L2 = sqrt(sum_sq))
+ *   max_abs  = max(max_abs, |(double)A_i - (double)B_i|)
+ * Accumulated sequentially in double; callers chain blocks through the
+ * in/out arguments. */
+void kvqo_recon_errors(const float *A, const float *B, int64_t n, double *sum_sq, double *max_abs)
+{
+    double ss = *sum_sq, mx = *max_abs;
+    for (int64_t i = 0; i < n; i++) {
+        double e = (double)A[i] - (double)B[i];
+        ss += e * e;
+        double ae = fabs(e);
+        if (ae > mx)
+            mx = ae;
+    }
+    *sum_sq = ss;
+    *max_abs = mx;
+}
+
+/* Raw dot-product scores S[i][t] = sum_d Q[i][d] * K[t][d] in double
+ * ("attention dot products"; reading Q10: no 1/sqrt(d_k), no softmax). */
+void kvqo_scores(const float *Q, int64_t nq, const float *K, int64_t T, int64_t D, double *S)
+{
+    for (int64_t i = 0; i < nq; i++)
+        for (int64_t t = 0; t < T; t++) {
+            double acc = 0.0;
+            for (int64_t d = 0; d < D; d++)
+                acc += (double)Q[i * D + d] * (double)K[t * D + d];
+            S[i * T + t] = acc;
+        }
+}
+
+/* Attention-score error (readings Q10, Q11):
+ *   returns sum_{i<nq, t<T} |S[i][t] - S'[i][t]|, S from K, S' from K_hat,
+ * each dot product accumulated in double.  mean = return / (nq * T). */
+double kvqo_attention_abs_sum(const float *Q, int64_t nq, const float *K, const float *K_hat,
+                              int64_t T, int64_t D)
+{
+    double total = 0.0;
+    for (int64_t i = 0; i < nq; i++)
+        for (int64_t t = 0; t < T; t++) {
+            double s = 0.0, sh = 0.0;
+            for (int64_t d = 0; d < D; d++) {
+                s += (double)Q[i * D + d] * (double)K[t * D + d];
+                sh += (double)Q[i * D + d] * (double)K_hat[t * D + d];
+            }
+            total += fabs(s - sh);
+        }
+    return total;
+}
+
+/* Theoretical max error max_d s_d / 2 (Eq. 9). */
+double kvqo_theoretical_max(const float *scales, int64_t D)
+{
+    double m = 0.0;
+    for (int64_t d = 0; d < D; d++)
+        if ((double)scales[d] / 2.0 > m)
+            m = (double)scales[d] / 2.0;
+    return m;
+}
