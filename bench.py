@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""bench.py — per-channel INT8 KV-key quantization on B200 (arxiv 2601.04719).
+
+One "step" = one pass of the whole hot path over
+the workload, through the C ABI on the device-resident inputs:
+    kvq_compute_scales (a1 column abs-max, a7 all-reduce MAX when N > 1, a2 /127)
+    kvq_quantize       (a3)
+    kvq_dequantize     (a4)
+    kvq_error_metrics_async (a5 L2 / max-abs, a6 attention-score error, nq = 64)
+Workload: BASELINE.json configs[3] (C4: 131072 x 8192 fp32 keys = 1.07e9
+elements, 4.3 GB > the 126 MB L2, so no flush is needed), token-sharded over
+N ranks (strong scaling).  Rank 0 prints one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1..C4] [--impl kvq|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {  # BASELINE.json configs
+    "C1": dict(T=1024, D=128, nq=64, desc="keys 1024x128 fp32 (131K elements)"),
+    "C2": dict(T=8192, D=1024, nq=64, desc="keys 8192x1024 fp32 (8.4M elements), 64 queries"),
+    "C3": dict(T=32768, D=8192, nq=64, desc="keys 32768x8192 fp32 (268M elements)"),
+    "C4": dict(T=131072, D=8192, nq=64, desc="keys 131072x8192 fp32 (1.07B elements, 4.3 GB), token-sharded"),
+}
+METRIC = "quantize+dequantize elements/s and achieved HBM GB/s vs B200 peak at 1/2/4/8 GPUs"
+# Algorithmic bytes per element of each pass: what the method itself must move.
+BYTES = {"scales": 4, "quantize": 5, "dequantize": 5, "metrics": 8}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return dict(hbm_gbs=j["hbm_gbs"], bf16_tflops=j["bf16_tflops"], sm_max_mhz=j.get("sm_max_mhz", 1965),
+                    source="measured (MEASURED_PEAKS.json)")
+    return dict(hbm_gbs=6650.0, bf16_tflops=1590.0, sm_max_mhz=1965, source="fallback (B200_PROFILING.md)")
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    QUERY = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self, t0=None, t1=None):
+        """Median SM clock and active throttle reasons over the samples taken
+        inside the wall-clock window [t0, t1] (the timed region)."""
+        import datetime
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 10:
+                continue
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                clk, cmax = float(f[2]), float(f[3])
+            except ValueError:
+                continue
+            if t0 is not None and not (t0 - 0.05 <= ts <= t1 + 0.05):
+                continue
+            sm.append(clk)
+            mx = cmax
+            for n, v in zip(names, f[6:10]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle (baseline / reference arm)
+def oracle_step(cfg, rows: int):
+    """The oracle as it stands on the first `rows` rows of the workload:
+    scales + quantize + dequantize + L2/max + attention error (nq queries).
+    Returns (seconds, elements).  Generation is excluded."""
+    import oracle
+    D, nq = cfg["D"], cfg["nq"]
+    K = oracle.fill(rows, D, oracle.SEED_K)
+    Q = oracle.fill(nq, D, oracle.SEED_Q)
+    t0 = time.perf_counter()
+    s = oracle.compute_scales(K)
+    q = oracle.quantize(K, s)
+    Kh = oracle.dequantize(q, s)
+    oracle.recon_errors(K, Kh)
+    oracle.attention_abs_sum(Q, K, Kh)
+    return time.perf_counter() - t0, rows * D
+
+
+def oracle_rows_for(cfg, seconds: float) -> int:
+    t, n = oracle_step(cfg, 8)
+    per_row = t / 8
+    return max(8, min(cfg["T"], int(seconds / per_row)))
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the oracle (plain C, single thread) is this tier's reference arm."""
+    if rank != 0:
+        return
+    rows = oracle_rows_for(cfg, 0.5 if args.steps * 1 <= 200 else 0.2)
+    for _ in range(args.warmup):
+        oracle_step(cfg, rows)
+    ts = []
+    for _ in range(args.steps):
+        t, n = oracle_step(cfg, rows)
+        ts.append(t)
+    tot = sum(ts)
+    value = rows * cfg["D"] * args.steps / tot
+    sample = f"first {rows} rows of {cfg['name']} ({rows}x{cfg['D']} elements) per step, nq={cfg['nq']}"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (splitmix64 lattice uniform [-1,1), SURVEY §8(d))",
+            "config": {"workload": cfg["desc"], "T": cfg["T"], "D": cfg["D"], "nq": cfg["nq"]},
+            "cpu_baseline": {"value": value, "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- the GPU arm
+def run_kvq(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_04719_b200 import kvq
+    from paper_2601_04719_b200.dist import make_comm, max_over_ranks, shard_rows
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    kvq.kvq_device_check()
+    T, D, nq = cfg["T"], cfg["D"], cfg["nq"]
+    row0, rows = shard_rows(T, world, rank)
+    comm = make_comm(rank, world) if world > 1 else None
+    stream = torch.cuda.current_stream()
+
+    # device-resident inputs (generated on the GPU by the seeded counter RNG; rank r makes its rows)
+    K = kvq.kvq_synth_fill(rows, D, row0=row0, seed=42, device=dev)
+    Q = kvq.kvq_synth_fill(nq, D, seed=43, device=dev)
+    scales = torch.empty(D, dtype=torch.float32, device=dev)
+    Kq = torch.empty((rows, D), dtype=torch.int8, device=dev)
+    Kh = torch.empty((rows, D), dtype=torch.float32, device=dev)
+    ws = torch.empty(kvq.kvq_error_metrics_workspace_size(rows, D, nq), dtype=torch.uint8, device=dev)
+    mout = torch.empty(kvq.METRICS_BYTES, dtype=torch.uint8, device=dev)
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        kvq.kvq_compute_scales(K, scales, comm=comm, stream=stream)
+        if ev is not None:
+            ev[1].record(stream)
+        kvq.kvq_quantize(K, scales, Kq, stream=stream)
+        if ev is not None:
+            ev[2].record(stream)
+        kvq.kvq_dequantize(Kq, scales, Kh, stream=stream)
+        if ev is not None:
+            ev[3].record(stream)
+        kvq.kvq_error_metrics_async(K, Kh, Q, scales, out_dev=mout, workspace=ws, comm=comm, stream=stream)
+        if ev is not None:
+            ev[4].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        wall0 = time.time()
+        start.record(stream)
+        for i in range(args.steps):
+            step(evs[i] if args.pass_events else None)
+        end.record(stream)
+        torch.cuda.synchronize()
+        wall1 = time.time()
+    if world > 1:
+        dist.barrier()
+    ms_local = start.elapsed_time(end) / args.steps
+    ms = max_over_ranks(ms_local, dev if world > 1 else None)
+    metrics = kvq.metrics_from_device(mout)
+
+    # per-pass device time (events on the launching stream), averaged over the timed steps
+    passes = {}
+    if args.pass_events:
+        names = ["scales", "quantize", "dequantize", "metrics"]
+        for j, nme in enumerate(names):
+            passes[nme] = statistics.mean(e[j].elapsed_time(e[j + 1]) for e in evs)
+    n_local = rows * D
+    pk = peaks()
+    pass_report = {}
+    for nme, t in passes.items():
+        gbs = BYTES[nme] * n_local / (t * 1e-3) / 1e9
+        pass_report[nme] = {"ms": t, "algo_bytes_per_elem": BYTES[nme], "GBps": gbs, "frac_hbm": gbs / pk["hbm_gbs"]}
+    dom = max(passes, key=passes.get) if passes else None
+
+    # ------------------------------------------------------------------ end to end from pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        del Kq, Kh, ws
+        torch.cuda.empty_cache()
+        Kh_host = K.cpu().pin_memory()
+        Qh_host = Q.cpu().pin_memory()
+        sc_h = torch.empty(D, dtype=torch.float32).pin_memory()
+        kq_h = torch.empty((rows, D), dtype=torch.int8).pin_memory()
+        wsz = kvq.kvq_roundtrip_host_workspace_size(rows, D, nq)
+        wsd = torch.empty(wsz, dtype=torch.uint8, device=dev)
+        del K
+        torch.cuda.empty_cache()
+        kvq.kvq_roundtrip_host(Kh_host, Qh_host, sc_h, kq_h, workspace=wsd, comm=comm, stream=stream)
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(e2e_steps):
+            r = kvq.kvq_roundtrip_host(Kh_host, Qh_host, sc_h, kq_h, workspace=wsd, comm=comm, stream=stream)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) / e2e_steps
+        e2e_ms = max_over_ranks(max(s0.elapsed_time(s1) / e2e_steps, wall * 1e3), dev if world > 1 else None)
+        e2e = {"value": T * D / (e2e_ms * 1e-3), "unit": "elements/s",
+               "h2d_bytes_per_step": rows * D * 4 + nq * D * 4,
+               "d2h_bytes_per_step": rows * D + D * 4 + kvq.METRICS_BYTES, "ms_per_step": e2e_ms,
+               "steps": e2e_steps, "api": "kvq_roundtrip_host (pinned host K/Q -> scales, codes, metrics)",
+               "attn_mean_abs": r["metrics"]["attn_mean_abs"]}
+
+    if rank != 0:
+        return
+    value = T * D / (ms * 1e-3)
+    algo_bytes = sum(BYTES.values()) * T * D
+    roofline = None
+    if dom:
+        t = passes[dom]
+        ach = BYTES[dom] * n_local / (t * 1e-3) / 1e9
+        roofline = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": ach / pk["hbm_gbs"], "traffic": None, "peak_source": pk["source"],
+                    "algo_bytes_per_elem": BYTES[dom], "ms_per_launch": t}
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        rows_cpu = oracle_rows_for(cfg, args.cpu_seconds)
+        t_cpu, n_cpu = oracle_step(cfg, rows_cpu)
+        cpu = {"value": n_cpu / t_cpu, "unit": "elements/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {rows_cpu} rows of {cfg['name']} ({n_cpu} elements): scales+quantize+dequantize"
+                         f"+L2/max+attention(nq={nq}), plain C single thread, generation excluded",
+               "seconds": t_cpu}
+    line = {
+        "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (splitmix64 lattice uniform [-1,1), SURVEY §8(d))",
+        "config": {"workload": f"{cfg['name']}: {cfg['desc']}", "T": T, "D": D, "nq": nq,
+                   "step": "compute_scales(+allreduce MAX) -> quantize -> dequantize -> error_metrics(L2,max,attn)",
+                   "l2_flush": "none needed: inputs larger than L2 (K alone is %.2f GB > 126 MB)" % (4 * T * D / 1e9)
+                   if 4 * T * D > 2 * 126e6 else "inputs L2-resident (warm)",
+                   "parallelism": f"token-shard x{world}"},
+        "hbm": {"GBps": algo_bytes / (ms * 1e-3) / 1e9 / world, "algo_bytes_per_elem": sum(BYTES.values()),
+                "frac_of_peak_per_gpu": algo_bytes / (ms * 1e-3) / 1e9 / world / pk["hbm_gbs"]},
+        "passes": pass_report, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": 7 * args.steps, "clocks": clk.summary(wall0, wall1),
+        "fidelity": {k: metrics[k] for k in ("l2", "max_abs", "attn_mean_abs", "theoretical_max")},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="kvq", choices=["kvq", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-pass-events", dest="pass_events", action="store_false")
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference", "need >= 3 warm-up steps"
+    cfg = dict(CONFIGS[args.config], name=args.config)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_kvq(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,157 @@
+/*
+ * kvq.h — C ABI of libkvq.so: per-channel symmetric INT8 quantization of an
+ * FP32 KV-cache key matrix on NVIDIA B200 (sm_100a), after arxiv 2601.04719.
+ *
+ * Citations: P:<line> = PAPER.md, S:<line> = SPEC.md (read-only reference),
+ * readings Q1..Q16 = DESIGN.md §3 (= SURVEY.md §8(c)).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Matrices are dense row-major [T][D]: K and K_hat are float32,
+ *    Kq is int8; element (t, d) lives at index t*D + d.  T is tokens, D is the
+ *    head dimension, one scale per column d.
+ *  - Pointers are CUDA device pointers on the current device unless marked
+ *    [host].  The caller owns every buffer; the library never allocates or
+ *    frees caller memory.  Any alignment is accepted: 16-byte aligned bases
+ *    with D % 4 == 0 take the 128-bit vector path, everything else an in-kernel
+ *    scalar path with bit-identical results.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Every call is asynchronous on `stream` unless documented otherwise.
+ *  - Argument errors are detected synchronously, return KVQ_ERR_INVALID_VALUE
+ *    and touch no output.  Launch failures return KVQ_ERR_CUDA; NCCL failures
+ *    KVQ_ERR_NCCL.  Device faults surface at the caller's next synchronization.
+ *    kvq_last_error() gives a thread-local message for the last failure.
+ *  - Input must be finite (reading Q7).  A column containing Inf/NaN
+ *    yields an Inf/NaN scale (visible without a sync); its codes are unspecified.
+ *  - Results are deterministic: codes, scales and K_hat are bit-identical run
+ *    to run, across launch geometries and across 1..N token-sharded ranks.
+ *  - There is no CPU fallback.  On a device other than sm_100 every compute
+ *    entry point returns KVQ_ERR_UNSUPPORTED.
+ */
+#ifndef KVQ_H
+#define KVQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVQ_ABI_VERSION 1
+
+typedef enum {
+    KVQ_OK = 0,
+    KVQ_ERR_INVALID_VALUE = 1, /* NULL pointer, T < 1, D < 1, T*D > 2^62, nq < 0, aliasing, short workspace */
+    KVQ_ERR_CUDA = 2,          /* CUDA runtime / launch error */
+    KVQ_ERR_NCCL = 3,          /* NCCL error, or NCCL not loadable */
+    KVQ_ERR_UNSUPPORTED = 4    /* current device is not sm_100 */
+} kvq_status;
+
+/* Opaque multi-GPU communicator (wraps an ncclComm_t; NULL = single GPU). */
+typedef struct kvq_comm_s *kvq_comm_t;
+
+/* Result of the paper's fidelity checks. */
+typedef struct {
+    double l2;              /* sqrt(sum (K - K_hat)^2), unnormalised Frobenius norm (reading Q9) */
+    double max_abs;         /* max |K - K_hat| */
+    double attn_mean_abs;   /* mean_{i<nq,t<T} |Q_i.K_t - Q_i.K_hat_t|, raw dot products (Q10/Q11); 0 if nq == 0 */
+    double theoretical_max; /* max_d s_d / 2 (Eq. 9); 0 if scales == NULL */
+    double sum_sq;          /* sum (K - K_hat)^2 (l2^2, kept for combination across calls) */
+    double attn_abs_sum;    /* sum_{i,t} |Q_i.K_t - Q_i.K_hat_t| */
+    int64_t n_elems;        /* T*D over all ranks */
+    int64_t n_scores;       /* nq*T over all ranks */
+} kvq_metrics;
+
+/* ---------------------------------------------------------------- utilities */
+int kvq_abi_version(void);
+const char *kvq_status_string(kvq_status s);
+/* Thread-local detail for the last non-OK status returned on this thread. */
+const char *kvq_last_error(void);
+/* KVQ_OK iff the current CUDA device is sm_100 (B200) and a kernel image loads. */
+kvq_status kvq_device_check(void);
+
+/* ---------------------------------------------------------------- multi-GPU */
+/* [host] out: 128 bytes (an ncclUniqueId).  Call on one rank, broadcast the bytes. */
+kvq_status kvq_comm_unique_id(void *out_id128);
+/* Collective over `nranks` processes (one GPU each, current device).  id: [host] 128 B. */
+kvq_status kvq_comm_init(kvq_comm_t *out, const void *id128, int nranks, int rank);
+kvq_status kvq_comm_destroy(kvq_comm_t comm);
+
+/* ---------------------------------------------------------------- the hot path */
+/* a1+a2(+a7): per-channel scales, Alg. 1, Eq. 6:
+ *   scales[d] = (max_t |K[t,d]|) / 127.0f       (fp32 IEEE division, reading Q3)
+ * K: [T][D] float32 in.  scales: [D] float32 out (also used as uint32 scratch
+ * while the max is formed; must not alias K).
+ * comm != NULL: K is this rank's token shard (rows of the global matrix); the
+ * column max is all-reduced (MAX) over ranks before the division, so scales
+ * come out global and identical on all ranks.  Must then be called by every
+ * rank of `comm` in the same order (NCCL rule). */
+kvq_status kvq_compute_scales(const float *K, int64_t T, int64_t D, float *scales,
+                              kvq_comm_t comm, void *stream);
+
+/* a3: Eq. 7 / Listing 3:
+ *   Kq[t,d] = clamp(round_half_even(fl32(K[t,d] / scales[d])), -127, 127),
+ *   and 0 where scales[d] == 0                   (readings Q1, Q2, Q4, Q5)
+ * K: [T][D] float32 in; scales: [D] in; Kq: [T][D] int8 out (may not alias K). */
+kvq_status kvq_quantize(const float *K, const float *scales, int64_t T, int64_t D,
+                        int8_t *Kq, void *stream);
+
+/* a4: Eq. 8 / Listing 4:
+ *   K_hat[t,d] = (float)Kq[t,d] * scales[d]      (one fp32 multiply; never -0)
+ * Kq: [T][D] int8 in; scales: [D] in; K_hat: [T][D] float32 out (may not alias Kq). */
+kvq_status kvq_dequantize(const int8_t *Kq, const float *scales, int64_t T, int64_t D,
+                          float *K_hat, void *stream);
+
+/* a3+a4 fused in one pass over K (9 B/elem instead of 10): writes both Kq and
+ * K_hat, bit-identical to kvq_quantize followed by kvq_dequantize. */
+kvq_status kvq_quantize_dequantize(const float *K, const float *scales, int64_t T, int64_t D,
+                                   int8_t *Kq, float *K_hat, void *stream);
+
+/* a5+a6: the paper's fidelity checks.
+ * K, K_hat: [T][D] float32 in.  Q: [nq][D] float32 queries or NULL (nq == 0).
+ * scales: [D] or NULL (only used for theoretical_max).  workspace: device
+ * scratch of at least kvq_error_metrics_workspace_size(T, D, nq) bytes.
+ * out_dev: DEVICE pointer to one kvq_metrics, written asynchronously.
+ * comm != NULL: K/K_hat are this rank's token shard; sums and maxima are
+ * all-reduced so every rank receives the global metrics.
+ * Accumulation is fp64 with a fixed reduction tree (deterministic). */
+size_t kvq_error_metrics_workspace_size(int64_t T, int64_t D, int64_t nq);
+kvq_status kvq_error_metrics_async(const float *K, const float *K_hat, int64_t T, int64_t D,
+                                   const float *Q, int64_t nq, const float *scales,
+                                   void *workspace, size_t workspace_bytes, kvq_comm_t comm,
+                                   kvq_metrics *out_dev, void *stream);
+/* Same, but out_host is [host] memory and the call synchronizes `stream`. */
+kvq_status kvq_error_metrics(const float *K, const float *K_hat, int64_t T, int64_t D,
+                             const float *Q, int64_t nq, const float *scales,
+                             void *workspace, size_t workspace_bytes, kvq_comm_t comm,
+                             kvq_metrics *out_host, void *stream);
+
+/* Raw attention scores for parity checks of a6 (reading Q10):
+ *   K_hat == NULL:  S[i][t] = sum_d Q[i][d] * K[t][d]
+ *   K_hat != NULL:  S[i][t] = sum_d Q[i][d] * (K[t][d] - K_hat[t][d])   (= S - S')
+ * Q: [nq][D], K/K_hat: [T][D], S: [nq][T] float32 out; fp32 products with
+ * per-32-term fp32 partial sums carried in fp64. */
+kvq_status kvq_attention_scores(const float *Q, int64_t nq, const float *K, const float *K_hat,
+                                int64_t T, int64_t D, float *S, void *stream);
+
+/* ---------------------------------------------------------------- host-buffer pipeline */
+/* The whole path from HOST memory (the end-to-end call a user makes):
+ * H2D of K (row blocks, overlapped with the column-max kernel), scales,
+ * fused quantize+dequantize, metrics, then D2H of scales, codes and metrics
+ * (and K_hat if K_hat_host != NULL).  Synchronizes `stream`.
+ * K_host [T][D], Q_host [nq][D] or NULL, scales_host [D], Kq_host [T][D]:
+ * [host] buffers, pinned (cudaHostAlloc / torch pin_memory) for full speed.
+ * dev_workspace: device scratch of kvq_roundtrip_host_workspace_size() bytes. */
+size_t kvq_roundtrip_host_workspace_size(int64_t T, int64_t D, int64_t nq);
+kvq_status kvq_roundtrip_host(const float *K_host, int64_t T, int64_t D,
+                              const float *Q_host, int64_t nq,
+                              float *scales_host, int8_t *Kq_host, float *K_hat_host,
+                              kvq_metrics *metrics_host,
+                              void *dev_workspace, size_t workspace_bytes,
+                              kvq_comm_t comm, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVQ_H */

@@ -1,0 +1,349 @@
+// api.cu — the extern "C" entry points of libkvq.so (include/kvq.h):
+// argument validation, launch sequencing on the caller's stream, error mapping.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kvq_internal.h"
+
+namespace kvq {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+kvq_status fail(kvq_status st, const std::string &msg) {
+    set_error(msg);
+    return st;
+}
+
+kvq_status check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(KVQ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return KVQ_OK;
+}
+
+static kvq_status cuda_check(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) return fail(KVQ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return KVQ_OK;
+}
+
+__global__ void probe_kernel() {}
+
+namespace {
+constexpr int kMaxDevices = 64;
+std::mutex g_mu;
+int g_state[kMaxDevices];  // 0 unknown, 1 ok, 2 unsupported
+DeviceInfo g_info[kMaxDevices];
+cudaStream_t g_copy_stream[kMaxDevices];
+}  // namespace
+
+kvq_status device_ok() {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(KVQ_ERR_CUDA, std::string("no usable CUDA device: ") + cudaGetErrorString(e));
+    }
+    if (dev < 0 || dev >= kMaxDevices) return fail(KVQ_ERR_UNSUPPORTED, "device index out of range");
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_state[dev] == 0) {
+        cudaDeviceProp p;
+        if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(KVQ_ERR_CUDA, "cudaGetDeviceProperties failed");
+        }
+        g_info[dev] = DeviceInfo{dev, p.multiProcessorCount, p.major, p.minor};
+        cudaFuncAttributes fa;
+        bool image = cudaFuncGetAttributes(&fa, probe_kernel) == cudaSuccess;
+        cudaGetLastError();
+        g_state[dev] = (p.major == 10 && p.minor == 0 && image) ? 1 : 2;
+    }
+    if (g_state[dev] != 1)
+        return fail(KVQ_ERR_UNSUPPORTED, "libkvq.so is built for sm_100a (B200) only; current device cc " +
+                                             std::to_string(g_info[dev].cc_major) + "." +
+                                             std::to_string(g_info[dev].cc_minor));
+    return KVQ_OK;
+}
+
+const DeviceInfo &device_info() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return g_info[dev];
+}
+
+static cudaStream_t copy_stream() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_copy_stream[dev]) cudaStreamCreateWithFlags(&g_copy_stream[dev], cudaStreamNonBlocking);
+    return g_copy_stream[dev];
+}
+
+}  // namespace kvq
+
+using namespace kvq;
+
+// ------------------------------------------------------------------------------ validation helpers
+static bool bad_dims(int64_t T, int64_t D) { return T < 1 || D < 1 || T > (int64_t(1) << 62) / D; }
+
+static bool overlap(const void *a, size_t na, const void *b, size_t nb) {
+    if (!a || !b) return false;
+    uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + nb && y < x + na;
+}
+
+#define KVQ_REQUIRE(cond, msg) \
+    do {                       \
+        if (!(cond)) return fail(KVQ_ERR_INVALID_VALUE, msg); \
+    } while (0)
+
+#define KVQ_TRY(expr)                       \
+    do {                                    \
+        kvq_status _st = (expr);            \
+        if (_st != KVQ_OK) return _st;      \
+    } while (0)
+
+// ------------------------------------------------------------------------------ utilities
+extern "C" int kvq_abi_version(void) { return KVQ_ABI_VERSION; }
+
+extern "C" const char *kvq_status_string(kvq_status s) {
+    switch (s) {
+        case KVQ_OK: return "KVQ_OK";
+        case KVQ_ERR_INVALID_VALUE: return "KVQ_ERR_INVALID_VALUE";
+        case KVQ_ERR_CUDA: return "KVQ_ERR_CUDA";
+        case KVQ_ERR_NCCL: return "KVQ_ERR_NCCL";
+        case KVQ_ERR_UNSUPPORTED: return "KVQ_ERR_UNSUPPORTED";
+    }
+    return "KVQ_ERR_UNKNOWN";
+}
+
+extern "C" const char *kvq_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" kvq_status kvq_device_check(void) { return device_ok(); }
+
+// ------------------------------------------------------------------------------ a1 + a2 (+ a7)
+extern "C" kvq_status kvq_compute_scales(const float *K, int64_t T, int64_t D, float *scales, kvq_comm_t comm,
+                                         void *stream) {
+    KVQ_REQUIRE(K && scales, "kvq_compute_scales: NULL pointer");
+    KVQ_REQUIRE(!bad_dims(T, D), "kvq_compute_scales: need T >= 1, D >= 1, T*D <= 2^62");
+    KVQ_REQUIRE(!overlap(K, (size_t)(T * D) * 4, scales, (size_t)D * 4), "kvq_compute_scales: scales aliases K");
+    KVQ_TRY(device_ok());
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t *bits = reinterpret_cast<uint32_t *>(scales);
+    KVQ_TRY(cuda_check(cudaMemsetAsync(bits, 0, (size_t)D * 4, s), "memset scales"));
+    KVQ_TRY(launch_colmax(K, T, D, bits, s));
+    if (comm) KVQ_TRY(comm_allreduce_max_u32(comm, bits, (size_t)D, s));
+    return launch_finalize(bits, D, s);
+}
+
+// ------------------------------------------------------------------------------ a3, a4
+static kvq_status quant_common(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq, float *K_hat,
+                               void *stream, const char *name) {
+    KVQ_REQUIRE(K && scales && Kq, std::string(name) + ": NULL pointer");
+    KVQ_REQUIRE(!bad_dims(T, D), std::string(name) + ": need T >= 1, D >= 1, T*D <= 2^62");
+    const size_t n = (size_t)(T * D);
+    KVQ_REQUIRE(!overlap(K, n * 4, Kq, n), std::string(name) + ": Kq aliases K");
+    KVQ_REQUIRE(!overlap(scales, (size_t)D * 4, Kq, n), std::string(name) + ": Kq aliases scales");
+    if (K_hat) {
+        KVQ_REQUIRE(!overlap(K_hat, n * 4, K, n * 4) && !overlap(K_hat, n * 4, Kq, n) &&
+                        !overlap(K_hat, n * 4, scales, (size_t)D * 4),
+                    std::string(name) + ": K_hat aliases an input");
+    }
+    KVQ_TRY(device_ok());
+    return launch_quantize(K, scales, T, D, Kq, K_hat, (cudaStream_t)stream);
+}
+
+extern "C" kvq_status kvq_quantize(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
+                                   void *stream) {
+    return quant_common(K, scales, T, D, Kq, nullptr, stream, "kvq_quantize");
+}
+
+extern "C" kvq_status kvq_quantize_dequantize(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
+                                              float *K_hat, void *stream) {
+    KVQ_REQUIRE(K_hat, "kvq_quantize_dequantize: NULL K_hat");
+    return quant_common(K, scales, T, D, Kq, K_hat, stream, "kvq_quantize_dequantize");
+}
+
+extern "C" kvq_status kvq_dequantize(const int8_t *Kq, const float *scales, int64_t T, int64_t D, float *K_hat,
+                                     void *stream) {
+    KVQ_REQUIRE(Kq && scales && K_hat, "kvq_dequantize: NULL pointer");
+    KVQ_REQUIRE(!bad_dims(T, D), "kvq_dequantize: need T >= 1, D >= 1, T*D <= 2^62");
+    const size_t n = (size_t)(T * D);
+    KVQ_REQUIRE(!overlap(K_hat, n * 4, Kq, n) && !overlap(K_hat, n * 4, scales, (size_t)D * 4),
+                "kvq_dequantize: K_hat aliases an input");
+    KVQ_TRY(device_ok());
+    return launch_dequantize(Kq, scales, T, D, K_hat, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------------------ a5 + a6
+extern "C" size_t kvq_error_metrics_workspace_size(int64_t T, int64_t D, int64_t nq) {
+    if (bad_dims(T, D) || nq < 0) return 0;
+    return metrics_workspace_size(T, D, nq) + 512;  // +512: device copy of the result for kvq_error_metrics
+}
+
+extern "C" kvq_status kvq_error_metrics_async(const float *K, const float *K_hat, int64_t T, int64_t D,
+                                              const float *Q, int64_t nq, const float *scales, void *workspace,
+                                              size_t workspace_bytes, kvq_comm_t comm, kvq_metrics *out_dev,
+                                              void *stream) {
+    KVQ_REQUIRE(K && K_hat && workspace && out_dev, "kvq_error_metrics: NULL pointer");
+    KVQ_REQUIRE(!bad_dims(T, D), "kvq_error_metrics: need T >= 1, D >= 1, T*D <= 2^62");
+    KVQ_REQUIRE(nq >= 0 && (nq == 0 || Q), "kvq_error_metrics: need nq >= 0 and Q when nq > 0");
+    KVQ_REQUIRE(nq <= (int64_t(1) << 62) / D && nq <= (int64_t(1) << 62) / T, "kvq_error_metrics: nq too large");
+    KVQ_REQUIRE(workspace_bytes >= metrics_workspace_size(T, D, nq), "kvq_error_metrics: workspace too small");
+    KVQ_TRY(device_ok());
+    cudaStream_t s = (cudaStream_t)stream;
+    MetricTotals tot;
+    KVQ_TRY(launch_metrics_partials(K, K_hat, T, D, nq ? Q : nullptr, nq, scales, workspace, workspace_bytes, &tot,
+                                    s));
+    if (comm) {
+        KVQ_TRY(comm_allreduce_sum_f64(comm, tot.sums, 4, s));
+        KVQ_TRY(comm_allreduce_max_u64(comm, tot.maxes, 2, s));
+    }
+    return launch_metrics_finalize(tot, out_dev, s);
+}
+
+extern "C" kvq_status kvq_error_metrics(const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
+                                        int64_t nq, const float *scales, void *workspace, size_t workspace_bytes,
+                                        kvq_comm_t comm, kvq_metrics *out_host, void *stream) {
+    KVQ_REQUIRE(out_host, "kvq_error_metrics: NULL out_host");
+    KVQ_REQUIRE(workspace && workspace_bytes >= 512 + 64, "kvq_error_metrics: workspace too small");
+    // The device copy of the result lives in the last 512 bytes of the workspace.
+    uintptr_t tail = ((uintptr_t)workspace + workspace_bytes - 512 + 63) & ~(uintptr_t)63;
+    kvq_metrics *dev_out = reinterpret_cast<kvq_metrics *>(tail);
+    KVQ_TRY(kvq_error_metrics_async(K, K_hat, T, D, Q, nq, scales, workspace, workspace_bytes - 512, comm, dev_out,
+                                    stream));
+    cudaStream_t s = (cudaStream_t)stream;
+    KVQ_TRY(cuda_check(cudaMemcpyAsync(out_host, dev_out, sizeof(kvq_metrics), cudaMemcpyDeviceToHost, s),
+                       "copy metrics"));
+    return cuda_check(cudaStreamSynchronize(s), "sync metrics");
+}
+
+extern "C" kvq_status kvq_attention_scores(const float *Q, int64_t nq, const float *K, const float *K_hat, int64_t T,
+                                           int64_t D, float *S, void *stream) {
+    KVQ_REQUIRE(Q && K && S, "kvq_attention_scores: NULL pointer");
+    KVQ_REQUIRE(!bad_dims(T, D) && nq >= 1 && nq <= (int64_t(1) << 62) / T, "kvq_attention_scores: bad sizes");
+    KVQ_TRY(device_ok());
+    return launch_attention_scores(Q, nq, K, K_hat, T, D, S, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------------------ host-buffer pipeline
+namespace {
+struct HostLayout {
+    size_t K, Kh, Kq, scales, Q, mws, mout, total;
+};
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+HostLayout host_layout(int64_t T, int64_t D, int64_t nq) {
+    HostLayout L;
+    const size_t n = (size_t)(T * D);
+    size_t off = 0;
+    L.K = off; off += al(n * 4);
+    L.Kh = off; off += al(n * 4);
+    L.Kq = off; off += al(n);
+    L.scales = off; off += al((size_t)D * 4);
+    L.Q = off; off += al((size_t)(nq * D) * 4);
+    L.mws = off; off += al(metrics_workspace_size(T, D, nq));
+    L.mout = off; off += al(sizeof(kvq_metrics));
+    L.total = off + 256;  // base alignment slack
+    return L;
+}
+}  // namespace
+
+extern "C" size_t kvq_roundtrip_host_workspace_size(int64_t T, int64_t D, int64_t nq) {
+    if (bad_dims(T, D) || nq < 0) return 0;
+    return host_layout(T, D, nq).total;
+}
+
+extern "C" kvq_status kvq_roundtrip_host(const float *K_host, int64_t T, int64_t D, const float *Q_host, int64_t nq,
+                                         float *scales_host, int8_t *Kq_host, float *K_hat_host,
+                                         kvq_metrics *metrics_host, void *dev_workspace, size_t workspace_bytes,
+                                         kvq_comm_t comm, void *stream) {
+    KVQ_REQUIRE(K_host && scales_host && Kq_host && metrics_host && dev_workspace,
+                "kvq_roundtrip_host: NULL pointer");
+    KVQ_REQUIRE(!bad_dims(T, D), "kvq_roundtrip_host: need T >= 1, D >= 1, T*D <= 2^62");
+    KVQ_REQUIRE(nq >= 0 && (nq == 0 || Q_host), "kvq_roundtrip_host: need nq >= 0 and Q when nq > 0");
+    const HostLayout L = host_layout(T, D, nq);
+    KVQ_REQUIRE(workspace_bytes >= L.total, "kvq_roundtrip_host: workspace too small");
+    KVQ_TRY(device_ok());
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaStream_t cs = copy_stream();
+    char *base = reinterpret_cast<char *>(((uintptr_t)dev_workspace + 255) & ~(uintptr_t)255);
+    float *K = reinterpret_cast<float *>(base + L.K);
+    float *Kh = reinterpret_cast<float *>(base + L.Kh);
+    int8_t *Kq = reinterpret_cast<int8_t *>(base + L.Kq);
+    float *sc = reinterpret_cast<float *>(base + L.scales);
+    float *Q = reinterpret_cast<float *>(base + L.Q);
+    kvq_metrics *mout = reinterpret_cast<kvq_metrics *>(base + L.mout);
+    uint32_t *bits = reinterpret_cast<uint32_t *>(sc);
+
+    // Row blocks of ~64 MB: block b's column-max kernel runs while block b+1 is in flight on the copy engine.
+    const size_t row_bytes = (size_t)D * 4;
+    int64_t rows_per = std::max<int64_t>(1, (int64_t)((64u << 20) / row_bytes));
+    int64_t nblk = (T + rows_per - 1) / rows_per;
+    if (nblk > 64) {
+        rows_per = (T + 63) / 64;
+        nblk = (T + rows_per - 1) / rows_per;
+    }
+    std::vector<cudaEvent_t> ev(nblk + 2);
+    for (auto &e : ev) KVQ_TRY(cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create"));
+    auto cleanup = [&]() {
+        for (auto &e : ev) cudaEventDestroy(e);
+    };
+    kvq_status st = KVQ_OK;
+    do {
+        // the copy stream must not overwrite the workspace before earlier work on `s` is done
+        if ((st = cuda_check(cudaEventRecord(ev[nblk], s), "record")) != KVQ_OK) break;
+        if ((st = cuda_check(cudaStreamWaitEvent(cs, ev[nblk], 0), "wait")) != KVQ_OK) break;
+        if ((st = cuda_check(cudaMemsetAsync(bits, 0, (size_t)D * 4, s), "memset")) != KVQ_OK) break;
+        for (int64_t b = 0; b < nblk && st == KVQ_OK; b++) {
+            const int64_t r0 = b * rows_per, nr = std::min(rows_per, T - r0);
+            st = cuda_check(cudaMemcpyAsync(K + r0 * D, K_host + r0 * D, (size_t)(nr * D) * 4,
+                                            cudaMemcpyHostToDevice, cs), "H2D K");
+            if (st == KVQ_OK) st = cuda_check(cudaEventRecord(ev[b], cs), "record");
+            if (st == KVQ_OK) st = cuda_check(cudaStreamWaitEvent(s, ev[b], 0), "wait");
+            if (st == KVQ_OK) st = launch_colmax(K + r0 * D, nr, D, bits, s);
+        }
+        if (st != KVQ_OK) break;
+        if (nq) {
+            if ((st = cuda_check(cudaMemcpyAsync(Q, Q_host, (size_t)(nq * D) * 4, cudaMemcpyHostToDevice, s),
+                                 "H2D Q")) != KVQ_OK)
+                break;
+        }
+        if (comm && (st = comm_allreduce_max_u32(comm, bits, (size_t)D, s)) != KVQ_OK) break;
+        if ((st = launch_finalize(bits, D, s)) != KVQ_OK) break;
+        if ((st = launch_quantize(K, sc, T, D, Kq, Kh, s)) != KVQ_OK) break;
+        // codes + scales (+ K_hat) go back on the copy engine while the metrics run on `s`
+        if ((st = cuda_check(cudaEventRecord(ev[nblk + 1], s), "record")) != KVQ_OK) break;
+        if ((st = cuda_check(cudaStreamWaitEvent(cs, ev[nblk + 1], 0), "wait")) != KVQ_OK) break;
+        if ((st = cuda_check(cudaMemcpyAsync(Kq_host, Kq, (size_t)(T * D), cudaMemcpyDeviceToHost, cs), "D2H Kq")) !=
+            KVQ_OK)
+            break;
+        if ((st = cuda_check(cudaMemcpyAsync(scales_host, sc, (size_t)D * 4, cudaMemcpyDeviceToHost, cs),
+                             "D2H scales")) != KVQ_OK)
+            break;
+        if (K_hat_host && (st = cuda_check(cudaMemcpyAsync(K_hat_host, Kh, (size_t)(T * D) * 4,
+                                                           cudaMemcpyDeviceToHost, cs),
+                                           "D2H K_hat")) != KVQ_OK)
+            break;
+        MetricTotals tot;
+        if ((st = launch_metrics_partials(K, Kh, T, D, nq ? Q : nullptr, nq, sc, base + L.mws,
+                                          metrics_workspace_size(T, D, nq), &tot, s)) != KVQ_OK)
+            break;
+        if (comm) {
+            if ((st = comm_allreduce_sum_f64(comm, tot.sums, 4, s)) != KVQ_OK) break;
+            if ((st = comm_allreduce_max_u64(comm, tot.maxes, 2, s)) != KVQ_OK) break;
+        }
+        if ((st = launch_metrics_finalize(tot, mout, s)) != KVQ_OK) break;
+        if ((st = cuda_check(cudaMemcpyAsync(metrics_host, mout, sizeof(kvq_metrics), cudaMemcpyDeviceToHost, s),
+                             "D2H metrics")) != KVQ_OK)
+            break;
+        if ((st = cuda_check(cudaStreamSynchronize(cs), "sync copy stream")) != KVQ_OK) break;
+        st = cuda_check(cudaStreamSynchronize(s), "sync stream");
+    } while (0);
+    cleanup();
+    return st;
+}

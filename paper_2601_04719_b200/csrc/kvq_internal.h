@@ -1,0 +1,67 @@
+// kvq_internal.h — internal (non-ABI) declarations shared by the libkvq.so
+// translation units.  Nothing here is exported; the ABI is include/kvq.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/kvq.h"
+
+namespace kvq {
+
+// Thread-local last-error message (kvq_last_error).
+void set_error(const std::string &msg);
+kvq_status fail(kvq_status st, const std::string &msg);
+kvq_status check_launch(const char *what);
+kvq_status device_ok();  // cached sm_100 check for the current device
+
+struct DeviceInfo {
+    int device;
+    int num_sms;
+    int cc_major, cc_minor;
+};
+const DeviceInfo &device_info();
+
+// Launch-geometry plan for the column-owning streaming kernels: G threads in
+// total, G a multiple of `cols` (element groups per row) so that every thread
+// owns fixed columns for the whole grid-stride loop (its scale and reciprocal
+// are loaded once; SURVEY §7 hard part (i)).
+struct StreamPlan {
+    int64_t G;        // total active threads (multiple of cols)
+    unsigned blocks;  // ceil(G / kThreads)
+};
+constexpr int kThreads = 256;
+StreamPlan plan_stream(int64_t rows, int64_t cols, int threads_per_sm);
+
+// ---- quantization kernels (quant_kernels.cu)
+kvq_status launch_colmax(const float *K, int64_t T, int64_t D, uint32_t *mbits, cudaStream_t s);
+kvq_status launch_finalize(uint32_t *mbits_to_scales, int64_t D, cudaStream_t s);
+kvq_status launch_quantize(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
+                           float *K_hat /* nullable: fused a3+a4 */, cudaStream_t s);
+kvq_status launch_dequantize(const int8_t *Kq, const float *scales, int64_t T, int64_t D, float *K_hat,
+                             cudaStream_t s);
+
+// ---- metrics kernels (metrics_kernels.cu)
+size_t metrics_workspace_size(int64_t T, int64_t D, int64_t nq);
+// Writes per-rank totals {sum_sq, attn_abs_sum, n_elems, n_scores} (double[4]) and
+// {max_abs_bits, theo_max_bits} (uint64[2]) into the workspace tail; returns
+// pointers to them so the comm layer can all-reduce in place.
+struct MetricTotals {
+    double *sums;      // [4] device
+    uint64_t *maxes;   // [2] device
+};
+kvq_status launch_metrics_partials(const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
+                                   int64_t nq, const float *scales, void *ws, size_t ws_bytes,
+                                   MetricTotals *totals, cudaStream_t s);
+kvq_status launch_metrics_finalize(const MetricTotals &totals, kvq_metrics *out_dev, cudaStream_t s);
+kvq_status launch_attention_scores(const float *Q, int64_t nq, const float *K, const float *K_hat, int64_t T,
+                                   int64_t D, float *S, cudaStream_t s);
+
+// ---- comm (comm.cpp)
+kvq_status comm_allreduce_max_u32(kvq_comm_t comm, uint32_t *buf, size_t count, cudaStream_t s);
+kvq_status comm_allreduce_sum_f64(kvq_comm_t comm, double *buf, size_t count, cudaStream_t s);
+kvq_status comm_allreduce_max_u64(kvq_comm_t comm, uint64_t *buf, size_t count, cudaStream_t s);
+
+}  // namespace kvq

@@ -1,0 +1,268 @@
+// metrics_kernels.cu — a5 reconstruction errors and a6 attention-score error
+// (P:20-24), plus raw scores for parity.
+//
+// One CTA owns a tile of 64 key rows and all queries.  It streams K and K_hat
+// across D in 32-column chunks, forms E = K - K_hat (exact in fp32, SURVEY
+// §8(c) fact 4), accumulates sum E^2 (fp64; each square is exact in fp64) and
+// max |E| (exact), and contracts E with the queries:
+//     Delta[i][t] = sum_d Q[i][d] * E[t][d]  ( = S - S' exactly in real arithmetic)
+// Computing the difference directly avoids the cancellation of S - S'
+// (|S| ~ 30, |S - S'| ~ 0.1 at D = 8192).  Each 32-term chunk is summed in
+// fp32 registers, chunks are carried in fp64, so the error is bounded by
+// ~32 u sum|Q E| instead of D u sum|Q E|.  Per-CTA partials are reduced by a
+// single CTA in a fixed order: metrics are deterministic run to run.
+#include <algorithm>
+
+#include "device_common.cuh"
+#include "kvq_internal.h"
+
+namespace kvq {
+
+constexpr int kTileRows = 64, kTileQ = 64, kChunk = 32, kPad = 68;
+
+struct Partial {
+    double sum_sq;
+    double attn_abs;
+    double max_abs;
+    double pad;
+};
+
+// MODE 0: metrics partials (E = K - K_hat).  MODE 1: write S (E = K or K - K_hat) to `S`.
+template <int MODE>
+__global__ void __launch_bounds__(256) attn_tile_kernel(const float *__restrict__ K, const float *__restrict__ Kh,
+                                                        const float *__restrict__ Q, int64_t T, int64_t D,
+                                                        int64_t nq, Partial *__restrict__ partials,
+                                                        float *__restrict__ S) {
+    __shared__ __align__(16) float Es[kChunk][kPad];
+    __shared__ __align__(16) float Qs[kChunk][kPad];
+    __shared__ double red[3][8];
+    const int tid = threadIdx.x;
+    const int ty = tid / 16, tx = tid % 16;  // compute mapping: rows ty*4.., queries tx*4..
+    const int lr = tid / 4, lk = (tid % 4) * 8;  // load mapping: row lr, columns lk..lk+7 of the chunk
+    const int64_t row0 = (int64_t)blockIdx.x * kTileRows;
+    const int64_t grow = row0 + lr;
+    const bool vec = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(K) | reinterpret_cast<uintptr_t>(Kh) |
+                                       reinterpret_cast<uintptr_t>(Q)) % 16 == 0);
+    double ss = 0.0, attn = 0.0;
+    float mx = 0.0f;
+    const int64_t nqt = nq > 0 ? (nq + kTileQ - 1) / kTileQ : 1;
+    for (int64_t qt = 0; qt < nqt; qt++) {
+        double dacc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) dacc[i][j] = 0.0;
+        const int64_t gq = qt * kTileQ + lr;  // query row loaded by this thread
+        for (int64_t k0 = 0; k0 < D; k0 += kChunk) {
+            // ---- load E chunk (64 rows x 32 cols) and Q chunk (64 queries x 32 cols)
+            float e[8], qv[8];
+            if (vec && k0 + lk + 8 <= D) {
+                float4 a0 = make_float4(0, 0, 0, 0), a1 = a0, b0 = a0, b1 = a0, c0 = a0, c1 = a0;
+                if (grow < T) {
+                    const float4 *kp = reinterpret_cast<const float4 *>(K + grow * D + k0 + lk);
+                    a0 = ld_stream_f4(kp);
+                    a1 = ld_stream_f4(kp + 1);
+                    if (Kh) {
+                        const float4 *hp = reinterpret_cast<const float4 *>(Kh + grow * D + k0 + lk);
+                        b0 = ld_stream_f4(hp);
+                        b1 = ld_stream_f4(hp + 1);
+                    }
+                }
+                if (nq > 0 && gq < nq) {
+                    const float4 *qp = reinterpret_cast<const float4 *>(Q + gq * D + k0 + lk);
+                    c0 = __ldg(qp);
+                    c1 = __ldg(qp + 1);
+                }
+                e[0] = a0.x - b0.x; e[1] = a0.y - b0.y; e[2] = a0.z - b0.z; e[3] = a0.w - b0.w;
+                e[4] = a1.x - b1.x; e[5] = a1.y - b1.y; e[6] = a1.z - b1.z; e[7] = a1.w - b1.w;
+                qv[0] = c0.x; qv[1] = c0.y; qv[2] = c0.z; qv[3] = c0.w;
+                qv[4] = c1.x; qv[5] = c1.y; qv[6] = c1.z; qv[7] = c1.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    const int64_t col = k0 + lk + j;
+                    float a = 0.0f, b = 0.0f, c = 0.0f;
+                    if (grow < T && col < D) {
+                        a = K[grow * D + col];
+                        if (Kh) b = Kh[grow * D + col];
+                    }
+                    if (nq > 0 && gq < nq && col < D) c = Q[gq * D + col];
+                    e[j] = a - b;
+                    qv[j] = c;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                if (MODE == 0 && qt == 0) {
+                    ss += (double)e[j] * (double)e[j];
+                    mx = fmaxf(mx, fabsf(e[j]));
+                }
+                Es[lk + j][lr] = e[j];
+                Qs[lk + j][lr] = qv[j];
+            }
+            __syncthreads();
+            if (nq > 0) {
+                float acc[4][4];
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) acc[i][j] = 0.0f;
+#pragma unroll 8
+                for (int k = 0; k < kChunk; k++) {
+                    const float4 a = *reinterpret_cast<const float4 *>(&Es[k][ty * 4]);
+                    const float4 b = *reinterpret_cast<const float4 *>(&Qs[k][tx * 4]);
+                    const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                    for (int i = 0; i < 4; i++)
+#pragma unroll
+                        for (int j = 0; j < 4; j++) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) dacc[i][j] += (double)acc[i][j];
+            }
+            __syncthreads();
+        }
+        if (nq > 0) {
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int64_t r = row0 + ty * 4 + i;
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const int64_t qi = qt * kTileQ + tx * 4 + j;
+                    if (r < T && qi < nq) {
+                        if (MODE == 0)
+                            attn += fabs(dacc[i][j]);
+                        else
+                            S[qi * T + r] = (float)dacc[i][j];
+                    }
+                }
+            }
+        }
+    }
+    if (MODE == 0) {
+        // fixed-order block reduction: warp shuffle tree, then warp 0 over the 8 warp results
+        double mxd = (double)mx;
+        for (int o = 16; o > 0; o >>= 1) {
+            ss += __shfl_xor_sync(0xffffffffu, ss, o);
+            attn += __shfl_xor_sync(0xffffffffu, attn, o);
+            mxd = fmax(mxd, __shfl_xor_sync(0xffffffffu, mxd, o));
+        }
+        const int w = tid / 32, l = tid % 32;
+        if (l == 0) {
+            red[0][w] = ss;
+            red[1][w] = attn;
+            red[2][w] = mxd;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            Partial p{0.0, 0.0, 0.0, 0.0};
+            for (int i = 0; i < 8; i++) {
+                p.sum_sq += red[0][i];
+                p.attn_abs += red[1][i];
+                p.max_abs = fmax(p.max_abs, red[2][i]);
+            }
+            partials[blockIdx.x] = p;
+        }
+    }
+}
+
+// Single CTA: fixed-order reduction of the per-tile partials, plus
+// theoretical_max = max_d s_d / 2 (Eq. 9) and the element counts.
+__global__ void __launch_bounds__(1024) reduce_partials_kernel(const Partial *__restrict__ partials, int64_t np,
+                                                               const float *__restrict__ scales, int64_t D,
+                                                               double n_elems, double n_scores, double *sums,
+                                                               uint64_t *maxes) {
+    __shared__ double sh[3][1024];
+    const int tid = threadIdx.x;
+    double ss = 0.0, at = 0.0, mx = 0.0, th = 0.0;
+    for (int64_t i = tid; i < np; i += 1024) {
+        ss += partials[i].sum_sq;
+        at += partials[i].attn_abs;
+        mx = fmax(mx, partials[i].max_abs);
+    }
+    if (scales)
+        for (int64_t d = tid; d < D; d += 1024) th = fmax(th, (double)scales[d] / 2.0);
+    sh[0][tid] = ss;
+    sh[1][tid] = at;
+    sh[2][tid] = fmax(mx, 0.0);
+    __syncthreads();
+    for (int s = 512; s > 0; s >>= 1) {
+        if (tid < s) {
+            sh[0][tid] += sh[0][tid + s];
+            sh[1][tid] += sh[1][tid + s];
+            sh[2][tid] = fmax(sh[2][tid], sh[2][tid + s]);
+        }
+        __syncthreads();
+    }
+    // theoretical max: separate max tree (reuse sh[2] after reading the max)
+    const double maxabs = sh[2][0];
+    __syncthreads();
+    sh[2][tid] = th;
+    __syncthreads();
+    for (int s = 512; s > 0; s >>= 1) {
+        if (tid < s) sh[2][tid] = fmax(sh[2][tid], sh[2][tid + s]);
+        __syncthreads();
+    }
+    if (tid == 0) {
+        sums[0] = sh[0][0];
+        sums[1] = sh[1][0];
+        sums[2] = n_elems;
+        sums[3] = n_scores;
+        maxes[0] = (uint64_t)__double_as_longlong(maxabs);
+        maxes[1] = (uint64_t)__double_as_longlong(sh[2][0]);
+    }
+}
+
+__global__ void metrics_finalize_kernel(const double *sums, const uint64_t *maxes, kvq_metrics *out) {
+    kvq_metrics m;
+    m.sum_sq = sums[0];
+    m.attn_abs_sum = sums[1];
+    m.n_elems = (int64_t)sums[2];
+    m.n_scores = (int64_t)sums[3];
+    m.l2 = sqrt(sums[0]);
+    m.max_abs = __longlong_as_double((long long)maxes[0]);
+    m.theoretical_max = __longlong_as_double((long long)maxes[1]);
+    m.attn_mean_abs = sums[3] > 0.0 ? sums[1] / sums[3] : 0.0;
+    *out = m;
+}
+
+// ---------------------------------------------------------------------------- host side
+static int64_t num_tiles(int64_t T) { return (T + kTileRows - 1) / kTileRows; }
+
+size_t metrics_workspace_size(int64_t T, int64_t D, int64_t nq) {
+    (void)D;
+    (void)nq;
+    return (size_t)num_tiles(T) * sizeof(Partial) + 4 * sizeof(double) + 2 * sizeof(uint64_t) + 256;
+}
+
+kvq_status launch_metrics_partials(const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
+                                   int64_t nq, const float *scales, void *ws, size_t ws_bytes,
+                                   MetricTotals *totals, cudaStream_t s) {
+    if (ws_bytes < metrics_workspace_size(T, D, nq))
+        return fail(KVQ_ERR_INVALID_VALUE, "error_metrics: workspace too small");
+    uintptr_t base = (reinterpret_cast<uintptr_t>(ws) + 255) & ~(uintptr_t)255;
+    Partial *partials = reinterpret_cast<Partial *>(base);
+    const int64_t nt = num_tiles(T);
+    totals->sums = reinterpret_cast<double *>(partials + nt);
+    totals->maxes = reinterpret_cast<uint64_t *>(totals->sums + 4);
+    attn_tile_kernel<0><<<(unsigned)nt, 256, 0, s>>>(K, K_hat, Q, T, D, nq, partials, nullptr);
+    if (kvq_status st = check_launch("metrics_tiles"); st != KVQ_OK) return st;
+    reduce_partials_kernel<<<1, 1024, 0, s>>>(partials, nt, scales, D, (double)T * (double)D,
+                                              (double)nq * (double)T, totals->sums, totals->maxes);
+    return check_launch("metrics_reduce");
+}
+
+kvq_status launch_metrics_finalize(const MetricTotals &t, kvq_metrics *out_dev, cudaStream_t s) {
+    metrics_finalize_kernel<<<1, 1, 0, s>>>(t.sums, t.maxes, out_dev);
+    return check_launch("metrics_finalize");
+}
+
+kvq_status launch_attention_scores(const float *Q, int64_t nq, const float *K, const float *K_hat, int64_t T,
+                                   int64_t D, float *S, cudaStream_t s) {
+    attn_tile_kernel<1><<<(unsigned)num_tiles(T), 256, 0, s>>>(K, K_hat, Q, T, D, nq, nullptr, S);
+    return check_launch("attention_scores");
+}
+
+}  // namespace kvq

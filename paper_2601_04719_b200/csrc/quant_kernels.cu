@@ -1,0 +1,348 @@
+// quant_kernels.cu — a1 column abs-max, a2 scale finalize, a3 quantize,
+// a4 dequantize (and a3+a4 fused) for sm_100a.
+//
+// All four are HBM-streaming kernels (arithmetic intensity ~1 op/byte), so the
+// design is about bytes in flight and instruction count, not tensor cores:
+//  * Column-owning grid-stride loops.  The flat float4 index space of K[T][D]
+//    is walked with a stride G that is a multiple of D/4, so each thread owns
+//    the same 4 columns for its whole life: scales, RN(1/s) and the running
+//    column max stay in registers (the paper's "coarsened" idea, P:320-347,
+//    with the vectorized kernel's 128-bit accesses).
+//  * U independent 128-bit loads in flight per thread (LDG.128, L1 no-allocate)
+//    and ~2048 resident threads per SM: >=128 KB of loads in flight per SM,
+//    well above the ~40 KB Little's-law requirement at 8 TB/s.
+//  * Codes are packed four per 32-bit store (P:365-370 char4), coalesced per warp.
+//  * Any D and any alignment: a scalar variant of every kernel (same geometry
+//    idea with stride a multiple of D) handles D % 4 != 0 or misaligned bases,
+//    which the paper's vectorized kernel leaves unwritten.
+#include <algorithm>
+
+#include "device_common.cuh"
+#include "kvq_internal.h"
+
+namespace kvq {
+
+// ============================================================================ a1: column abs-max
+// m_d = max_t |K[t,d]| as the uint32 max of (bits & 0x7fffffff): for finite
+// non-negative floats IEEE order equals integer order, and Inf/NaN propagate
+// (reading Q7).  Exact under any reduction order.
+template <int U>
+__global__ void __launch_bounds__(kThreads) colmax_v4_kernel(const float4 *__restrict__ K, int64_t n4,
+                                                             int64_t cols4, int64_t G,
+                                                             uint32_t *__restrict__ mbits) {
+    extern __shared__ uint32_t smax[];  // [4*cols4] when cols4 <= kThreads
+    const bool share = cols4 <= kThreads;
+    const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (share) {
+        for (int i = threadIdx.x; i < 4 * cols4; i += kThreads) smax[i] = 0u;
+        __syncthreads();
+    }
+    uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+    int64_t c4 = 0;
+    if (g < G) {
+        c4 = g % cols4;
+        int64_t i = g;
+        for (; i + (U - 1) * G < n4; i += U * G) {
+            float4 v[U];
+#pragma unroll
+            for (int k = 0; k < U; k++) v[k] = ld_stream_f4(K + i + k * G);
+#pragma unroll
+            for (int k = 0; k < U; k++) {
+                m0 = max(m0, absbits(v[k].x));
+                m1 = max(m1, absbits(v[k].y));
+                m2 = max(m2, absbits(v[k].z));
+                m3 = max(m3, absbits(v[k].w));
+            }
+        }
+        for (; i < n4; i += G) {
+            float4 v = ld_stream_f4(K + i);
+            m0 = max(m0, absbits(v.x));
+            m1 = max(m1, absbits(v.y));
+            m2 = max(m2, absbits(v.z));
+            m3 = max(m3, absbits(v.w));
+        }
+    }
+    if (share) {
+        if (g < G) {
+            atomicMax(&smax[4 * c4 + 0], m0);
+            atomicMax(&smax[4 * c4 + 1], m1);
+            atomicMax(&smax[4 * c4 + 2], m2);
+            atomicMax(&smax[4 * c4 + 3], m3);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < 4 * cols4; i += kThreads)
+            if (smax[i]) atomicMax(&mbits[i], smax[i]);
+    } else if (g < G) {
+        atomicMax(&mbits[4 * c4 + 0], m0);
+        atomicMax(&mbits[4 * c4 + 1], m1);
+        atomicMax(&mbits[4 * c4 + 2], m2);
+        atomicMax(&mbits[4 * c4 + 3], m3);
+    }
+}
+
+template <int U>
+__global__ void __launch_bounds__(kThreads) colmax_scalar_kernel(const float *__restrict__ K, int64_t n,
+                                                                 int64_t D, int64_t G,
+                                                                 uint32_t *__restrict__ mbits) {
+    const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (g >= G) return;
+    uint32_t m = 0;
+    int64_t i = g;
+    for (; i + (U - 1) * G < n; i += U * G) {
+        float v[U];
+#pragma unroll
+        for (int k = 0; k < U; k++) v[k] = __ldg(K + i + k * G);
+#pragma unroll
+        for (int k = 0; k < U; k++) m = max(m, absbits(v[k]));
+    }
+    for (; i < n; i += G) m = max(m, absbits(__ldg(K + i)));
+    if (m) atomicMax(&mbits[g % D], m);
+}
+
+// ============================================================================ a2: finalize
+// s_d = fl32(m_d / 127.0f), IEEE division (reading Q3); in place.
+__global__ void finalize_kernel(uint32_t *buf, int64_t D) {
+    for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < D; d += (int64_t)gridDim.x * blockDim.x) {
+        float m = __uint_as_float(buf[d]);
+        reinterpret_cast<float *>(buf)[d] = __fdiv_rn(m, 127.0f);
+    }
+}
+
+// ============================================================================ a3 (+a4): quantize
+template <bool FUSED>
+__device__ __forceinline__ void quant4(const float4 &x, const ColQ &q0, const ColQ &q1, const ColQ &q2,
+                                       const ColQ &q3, bool col_exact, uint32_t &w, float4 &xh) {
+    bool danger = col_exact;
+    float a0 = quant_fast(x.x, q0, danger);
+    float a1 = quant_fast(x.y, q1, danger);
+    float a2 = quant_fast(x.z, q2, danger);
+    float a3 = quant_fast(x.w, q3, danger);
+    if (__builtin_expect(!danger, 1)) {
+        w = pack4(a0, a1, a2, a3);
+        if (FUSED) {
+            xh.x = __fmul_rn(__fsub_rn(a0, kMagic), q0.s);
+            xh.y = __fmul_rn(__fsub_rn(a1, kMagic), q1.s);
+            xh.z = __fmul_rn(__fsub_rn(a2, kMagic), q2.s);
+            xh.w = __fmul_rn(__fsub_rn(a3, kMagic), q3.s);
+        }
+    } else {
+        int c0 = quant_exact(x.x, q0.s), c1 = quant_exact(x.y, q1.s);
+        int c2 = quant_exact(x.z, q2.s), c3 = quant_exact(x.w, q3.s);
+        w = (uint32_t)(c0 & 0xff) | ((uint32_t)(c1 & 0xff) << 8) | ((uint32_t)(c2 & 0xff) << 16) |
+            ((uint32_t)(c3 & 0xff) << 24);
+        if (FUSED) {
+            xh.x = __fmul_rn((float)c0, q0.s);
+            xh.y = __fmul_rn((float)c1, q1.s);
+            xh.z = __fmul_rn((float)c2, q2.s);
+            xh.w = __fmul_rn((float)c3, q3.s);
+        }
+    }
+}
+
+template <int U, bool FUSED>
+__global__ void __launch_bounds__(kThreads) quant_v4_kernel(const float4 *__restrict__ K,
+                                                            const float *__restrict__ scales,
+                                                            uint32_t *__restrict__ Kq4, float4 *__restrict__ Kh4,
+                                                            int64_t n4, int64_t cols4, int64_t G) {
+    const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (g >= G) return;
+    const int64_t c4 = g % cols4;
+    const ColQ q0 = make_colq(__ldg(scales + 4 * c4 + 0));
+    const ColQ q1 = make_colq(__ldg(scales + 4 * c4 + 1));
+    const ColQ q2 = make_colq(__ldg(scales + 4 * c4 + 2));
+    const ColQ q3 = make_colq(__ldg(scales + 4 * c4 + 3));
+    const bool col_exact = q0.exact | q1.exact | q2.exact | q3.exact;
+    for (int64_t i = g; i < n4; i += U * G) {
+        float4 v[U];
+#pragma unroll
+        for (int k = 0; k < U; k++)
+            if (i + k * G < n4) v[k] = ld_stream_f4(K + i + k * G);
+#pragma unroll
+        for (int k = 0; k < U; k++) {
+            const int64_t idx = i + k * G;
+            if (idx < n4) {
+                uint32_t w;
+                float4 xh;
+                quant4<FUSED>(v[k], q0, q1, q2, q3, col_exact, w, xh);
+                Kq4[idx] = w;
+                if (FUSED) Kh4[idx] = xh;
+            }
+        }
+    }
+}
+
+template <int U, bool FUSED>
+__global__ void __launch_bounds__(kThreads) quant_scalar_kernel(const float *__restrict__ K,
+                                                                const float *__restrict__ scales,
+                                                                int8_t *__restrict__ Kq, float *__restrict__ Kh,
+                                                                int64_t n, int64_t D, int64_t G) {
+    const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (g >= G) return;
+    const ColQ q = make_colq(__ldg(scales + g % D));
+    for (int64_t i = g; i < n; i += U * G) {
+        float v[U];
+#pragma unroll
+        for (int k = 0; k < U; k++)
+            if (i + k * G < n) v[k] = __ldg(K + i + k * G);
+#pragma unroll
+        for (int k = 0; k < U; k++) {
+            const int64_t idx = i + k * G;
+            if (idx < n) {
+                bool danger = q.exact;
+                float a = quant_fast(v[k], q, danger);
+                int c = danger ? quant_exact(v[k], q.s) : (int)(int8_t)code_byte(a);
+                Kq[idx] = (int8_t)c;
+                if (FUSED) Kh[idx] = __fmul_rn((float)c, q.s);
+            }
+        }
+    }
+}
+
+// ============================================================================ a4: dequantize
+// x_hat = fl32((float)q * s_d): one IEEE multiply; (float)0 * s = +0.
+template <int U>
+__global__ void __launch_bounds__(kThreads) dequant_v4_kernel(const uint32_t *__restrict__ Kq4,
+                                                              const float *__restrict__ scales,
+                                                              float4 *__restrict__ Kh4, int64_t n4,
+                                                              int64_t cols4, int64_t G) {
+    const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (g >= G) return;
+    const int64_t c4 = g % cols4;
+    const float s0 = __ldg(scales + 4 * c4 + 0), s1 = __ldg(scales + 4 * c4 + 1);
+    const float s2 = __ldg(scales + 4 * c4 + 2), s3 = __ldg(scales + 4 * c4 + 3);
+    for (int64_t i = g; i < n4; i += U * G) {
+        uint32_t w[U];
+#pragma unroll
+        for (int k = 0; k < U; k++)
+            if (i + k * G < n4) w[k] = ld_stream_u32(Kq4 + i + k * G);
+#pragma unroll
+        for (int k = 0; k < U; k++) {
+            const int64_t idx = i + k * G;
+            if (idx < n4) {
+                float4 o;
+                o.x = __fmul_rn(code_to_float(w[k], 0), s0);
+                o.y = __fmul_rn(code_to_float(w[k], 1), s1);
+                o.z = __fmul_rn(code_to_float(w[k], 2), s2);
+                o.w = __fmul_rn(code_to_float(w[k], 3), s3);
+                Kh4[idx] = o;
+            }
+        }
+    }
+}
+
+template <int U>
+__global__ void __launch_bounds__(kThreads) dequant_scalar_kernel(const int8_t *__restrict__ Kq,
+                                                                  const float *__restrict__ scales,
+                                                                  float *__restrict__ Kh, int64_t n, int64_t D,
+                                                                  int64_t G) {
+    const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (g >= G) return;
+    const float s = __ldg(scales + g % D);
+    for (int64_t i = g; i < n; i += U * G) {
+        int8_t c[U];
+#pragma unroll
+        for (int k = 0; k < U; k++)
+            if (i + k * G < n) c[k] = Kq[i + k * G];
+#pragma unroll
+        for (int k = 0; k < U; k++)
+            if (i + k * G < n) Kh[i + k * G] = __fmul_rn((float)(int)c[k], s);
+    }
+}
+
+// ============================================================================ host launchers
+static inline bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+StreamPlan plan_stream(int64_t rows, int64_t cols, int threads_per_sm) {
+    const DeviceInfo &di = device_info();
+    const int64_t target = (int64_t)di.num_sms * threads_per_sm;
+    int64_t R = std::max<int64_t>(1, target / cols);
+    R = std::min<int64_t>(R, rows);
+    StreamPlan p;
+    p.G = cols * R;
+    p.blocks = (unsigned)((p.G + kThreads - 1) / kThreads);
+    return p;
+}
+
+constexpr int kUColmax = 8, kUQuant = 4, kUDequant = 8;
+
+// Resident threads per SM for `kernel` at kThreads per CTA: the grid is sized
+// to exactly one full wave of resident threads (no tail wave).
+template <typename Kern>
+static int resident_threads(Kern kernel, size_t smem) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kThreads, smem) != cudaSuccess || nb < 1) {
+        cudaGetLastError();
+        nb = 1;
+    }
+    return nb * kThreads;
+}
+#define KVQ_RESIDENT(kernel, smem)                                     \
+    ([&]() {                                                           \
+        static const int r_ = resident_threads(kernel, (smem));        \
+        return r_;                                                     \
+    }())
+
+kvq_status launch_colmax(const float *K, int64_t T, int64_t D, uint32_t *mbits, cudaStream_t s) {
+    const int64_t n = T * D;
+    if (D % 4 == 0 && aligned(K, 16)) {
+        const int64_t cols4 = D / 4;
+        size_t smem = cols4 <= kThreads ? (size_t)4 * cols4 * sizeof(uint32_t) : 0;
+        StreamPlan p = plan_stream(T, cols4, KVQ_RESIDENT(colmax_v4_kernel<kUColmax>, 4 * kThreads * sizeof(uint32_t)));
+        colmax_v4_kernel<kUColmax><<<p.blocks, kThreads, smem, s>>>(reinterpret_cast<const float4 *>(K), n / 4,
+                                                                   cols4, p.G, mbits);
+    } else {
+        StreamPlan p = plan_stream(T, D, KVQ_RESIDENT(colmax_scalar_kernel<kUColmax>, 0));
+        colmax_scalar_kernel<kUColmax><<<p.blocks, kThreads, 0, s>>>(K, n, D, p.G, mbits);
+    }
+    return check_launch("colmax");
+}
+
+kvq_status launch_finalize(uint32_t *buf, int64_t D, cudaStream_t s) {
+    unsigned blocks = (unsigned)std::min<int64_t>((D + 255) / 256, 1024);
+    finalize_kernel<<<blocks, 256, 0, s>>>(buf, D);
+    return check_launch("finalize");
+}
+
+kvq_status launch_quantize(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq, float *K_hat,
+                           cudaStream_t s) {
+    const int64_t n = T * D;
+    const bool vec = D % 4 == 0 && aligned(K, 16) && aligned(Kq, 4) && (!K_hat || aligned(K_hat, 16));
+    if (vec) {
+        const int64_t cols4 = D / 4;
+        StreamPlan p = plan_stream(T, cols4, K_hat ? KVQ_RESIDENT((quant_v4_kernel<kUQuant, true>), 0)
+                                                   : KVQ_RESIDENT((quant_v4_kernel<kUQuant, false>), 0));
+        auto K4 = reinterpret_cast<const float4 *>(K);
+        auto Q4 = reinterpret_cast<uint32_t *>(Kq);
+        if (K_hat)
+            quant_v4_kernel<kUQuant, true><<<p.blocks, kThreads, 0, s>>>(K4, scales, Q4,
+                                                                         reinterpret_cast<float4 *>(K_hat), n / 4,
+                                                                         cols4, p.G);
+        else
+            quant_v4_kernel<kUQuant, false><<<p.blocks, kThreads, 0, s>>>(K4, scales, Q4, nullptr, n / 4, cols4,
+                                                                          p.G);
+    } else {
+        StreamPlan p = plan_stream(T, D, KVQ_RESIDENT((quant_scalar_kernel<kUQuant, true>), 0));
+        if (K_hat)
+            quant_scalar_kernel<kUQuant, true><<<p.blocks, kThreads, 0, s>>>(K, scales, Kq, K_hat, n, D, p.G);
+        else
+            quant_scalar_kernel<kUQuant, false><<<p.blocks, kThreads, 0, s>>>(K, scales, Kq, nullptr, n, D, p.G);
+    }
+    return check_launch(K_hat ? "quantize_dequantize" : "quantize");
+}
+
+kvq_status launch_dequantize(const int8_t *Kq, const float *scales, int64_t T, int64_t D, float *K_hat,
+                             cudaStream_t s) {
+    const int64_t n = T * D;
+    if (D % 4 == 0 && aligned(Kq, 4) && aligned(K_hat, 16)) {
+        const int64_t cols4 = D / 4;
+        StreamPlan p = plan_stream(T, cols4, KVQ_RESIDENT(dequant_v4_kernel<kUDequant>, 0));
+        dequant_v4_kernel<kUDequant><<<p.blocks, kThreads, 0, s>>>(
+            reinterpret_cast<const uint32_t *>(Kq), scales, reinterpret_cast<float4 *>(K_hat), n / 4, cols4, p.G);
+    } else {
+        StreamPlan p = plan_stream(T, D, KVQ_RESIDENT(dequant_scalar_kernel<kUDequant>, 0));
+        dequant_scalar_kernel<kUDequant><<<p.blocks, kThreads, 0, s>>>(Kq, scales, K_hat, n, D, p.G);
+    }
+    return check_launch("dequantize");
+}
+
+}  // namespace kvq

@@ -1,0 +1,55 @@
+"""Token-dimension sharding helpers.
+
+Rank r of R owns the contiguous row block [row0, row0+rows) of the global
+T x D key matrix.  The only exchange step of the method is the all-reduce MAX
+of the D column maxima inside kvq_compute_scales (done by libkvq.so over NCCL);
+everything here is host-side plumbing: the partition, the NCCL unique-id
+bootstrap over torch.distributed, and max-over-ranks timing.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_rows(T: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced row partition: the first T % world ranks get one extra row."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    base, extra = divmod(T, world)
+    row0 = rank * base + min(rank, extra)
+    return row0, base + (1 if rank < extra else 0)
+
+
+def broadcast_bytes(payload: bytes | None, src: int = 0, group=None) -> bytes:
+    """Broadcast a short byte string (e.g. a 128-byte ncclUniqueId) from `src`
+    to every rank of the default process group (works over gloo and nccl)."""
+    obj = [payload]
+    dist.broadcast_object_list(obj, src=src, group=group)
+    return obj[0]
+
+
+def max_over_ranks(x: float, device=None) -> float:
+    """Max of a per-rank scalar (device-timed milliseconds) over all ranks."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device or "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, device=None) -> float:
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device or "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def make_comm(rank: int, world: int):
+    """Create the library's NCCL communicator: rank 0 draws the unique id, the
+    default process group broadcasts it, every rank calls kvq_comm_init."""
+    from .kvq import Comm, kvq_comm_unique_id
+    uid = kvq_comm_unique_id() if rank == 0 else None
+    uid = broadcast_bytes(uid, src=0)
+    return Comm(uid, world, rank)

@@ -1,0 +1,236 @@
+"""Thin Python binding of libkvq.so with the same names as the C ABI
+(include/kvq.h).  Argument marshalling only: torch supplies device memory and
+streams, every step of the path runs in libkvq.so's kernels.  Tensors must be
+CUDA tensors on the current device (host tensors for the *_host call); there is
+no CPU fallback and a missing/unsupported GPU raises KvqError.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import torch
+
+from ._lib import KvqError, check, kvq_metrics, load
+
+__all__ = [
+    "KvqError", "Comm", "kvq_compute_scales", "kvq_quantize", "kvq_dequantize", "kvq_quantize_dequantize",
+    "kvq_error_metrics", "kvq_error_metrics_async", "kvq_error_metrics_workspace_size", "kvq_attention_scores",
+    "kvq_roundtrip_host", "kvq_roundtrip_host_workspace_size", "kvq_synth_fill", "kvq_device_check",
+    "kvq_comm_unique_id", "METRICS_BYTES", "metrics_from_device",
+]
+
+load()  # fail loudly at import if libkvq.so cannot be loaded or built
+
+METRICS_BYTES = ctypes.sizeof(kvq_metrics)
+DIST_UNIFORM, DIST_OUTLIER, DIST_ONGRID = 0, 1, 2
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _mat(t: torch.Tensor, dtype, name: str, cuda: bool = True):
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if t.dim() != 2:
+        raise ValueError(f"{name}: expected a [T, D] matrix, got shape {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous row-major")
+    if cuda and not t.is_cuda:
+        raise ValueError(f"{name}: must be a CUDA tensor (there is no CPU path)")
+    return t.shape[0], t.shape[1]
+
+
+def _vec(t: torch.Tensor, n: int, name: str):
+    if t.dtype != torch.float32 or t.numel() != n or not t.is_contiguous() or not t.is_cuda:
+        raise ValueError(f"{name}: expected contiguous CUDA float32[{n}]")
+
+
+def _comm_handle(comm):
+    return None if comm is None else comm.handle
+
+
+# ----------------------------------------------------------------------------- utilities
+def kvq_device_check() -> None:
+    check(load().kvq_device_check(), "kvq_device_check")
+
+
+def kvq_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(load().kvq_comm_unique_id(buf), "kvq_comm_unique_id")
+    return buf.raw
+
+
+class Comm:
+    """Owns a kvq_comm_t (an NCCL communicator over one GPU per process)."""
+
+    def __init__(self, unique_id: bytes, nranks: int, rank: int):
+        assert len(unique_id) == 128
+        h = ctypes.c_void_p()
+        idbuf = ctypes.create_string_buffer(unique_id, 128)
+        check(load().kvq_comm_init(ctypes.byref(h), idbuf, nranks, rank), "kvq_comm_init")
+        self.handle, self.nranks, self.rank = h, nranks, rank
+
+    def destroy(self):
+        if self.handle:
+            check(load().kvq_comm_destroy(self.handle), "kvq_comm_destroy")
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+# ----------------------------------------------------------------------------- the hot path
+def kvq_compute_scales(K: torch.Tensor, scales: Optional[torch.Tensor] = None, comm: Optional[Comm] = None,
+                       stream=None) -> torch.Tensor:
+    T, D = _mat(K, torch.float32, "K")
+    if scales is None:
+        scales = torch.empty(D, dtype=torch.float32, device=K.device)
+    _vec(scales, D, "scales")
+    check(load().kvq_compute_scales(_ptr(K), T, D, _ptr(scales), _comm_handle(comm), _stream(stream)),
+          "kvq_compute_scales")
+    return scales
+
+
+def kvq_quantize(K: torch.Tensor, scales: torch.Tensor, Kq: Optional[torch.Tensor] = None,
+                 stream=None) -> torch.Tensor:
+    T, D = _mat(K, torch.float32, "K")
+    _vec(scales, D, "scales")
+    if Kq is None:
+        Kq = torch.empty((T, D), dtype=torch.int8, device=K.device)
+    _mat(Kq, torch.int8, "Kq")
+    check(load().kvq_quantize(_ptr(K), _ptr(scales), T, D, _ptr(Kq), _stream(stream)), "kvq_quantize")
+    return Kq
+
+
+def kvq_dequantize(Kq: torch.Tensor, scales: torch.Tensor, K_hat: Optional[torch.Tensor] = None,
+                   stream=None) -> torch.Tensor:
+    T, D = _mat(Kq, torch.int8, "Kq")
+    _vec(scales, D, "scales")
+    if K_hat is None:
+        K_hat = torch.empty((T, D), dtype=torch.float32, device=Kq.device)
+    _mat(K_hat, torch.float32, "K_hat")
+    check(load().kvq_dequantize(_ptr(Kq), _ptr(scales), T, D, _ptr(K_hat), _stream(stream)), "kvq_dequantize")
+    return K_hat
+
+
+def kvq_quantize_dequantize(K: torch.Tensor, scales: torch.Tensor, Kq: Optional[torch.Tensor] = None,
+                            K_hat: Optional[torch.Tensor] = None, stream=None):
+    T, D = _mat(K, torch.float32, "K")
+    _vec(scales, D, "scales")
+    if Kq is None:
+        Kq = torch.empty((T, D), dtype=torch.int8, device=K.device)
+    if K_hat is None:
+        K_hat = torch.empty((T, D), dtype=torch.float32, device=K.device)
+    check(load().kvq_quantize_dequantize(_ptr(K), _ptr(scales), T, D, _ptr(Kq), _ptr(K_hat), _stream(stream)),
+          "kvq_quantize_dequantize")
+    return Kq, K_hat
+
+
+def kvq_error_metrics_workspace_size(T: int, D: int, nq: int) -> int:
+    return int(load().kvq_error_metrics_workspace_size(T, D, nq))
+
+
+def _metrics_args(K, K_hat, Q, scales, workspace):
+    T, D = _mat(K, torch.float32, "K")
+    _mat(K_hat, torch.float32, "K_hat")
+    nq = 0
+    if Q is not None:
+        nq, Dq = _mat(Q, torch.float32, "Q")
+        assert Dq == D
+    if scales is not None:
+        _vec(scales, D, "scales")
+    need = kvq_error_metrics_workspace_size(T, D, nq)
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=K.device)
+    assert workspace.numel() >= need, "workspace too small"
+    return T, D, nq, workspace
+
+
+def kvq_error_metrics_async(K, K_hat, Q=None, scales=None, out_dev: Optional[torch.Tensor] = None,
+                            workspace=None, comm: Optional[Comm] = None, stream=None) -> torch.Tensor:
+    """Writes a kvq_metrics struct into `out_dev` (uint8[METRICS_BYTES] on the device), asynchronously."""
+    T, D, nq, workspace = _metrics_args(K, K_hat, Q, scales, workspace)
+    if out_dev is None:
+        out_dev = torch.empty(METRICS_BYTES, dtype=torch.uint8, device=K.device)
+    check(load().kvq_error_metrics_async(_ptr(K), _ptr(K_hat), T, D, _ptr(Q), nq, _ptr(scales), _ptr(workspace),
+                                         workspace.numel(), _comm_handle(comm), _ptr(out_dev), _stream(stream)),
+          "kvq_error_metrics_async")
+    return out_dev
+
+
+def metrics_from_device(out_dev: torch.Tensor) -> dict:
+    raw = bytes(out_dev.cpu().numpy().tobytes())
+    return kvq_metrics.from_buffer_copy(raw).to_dict()
+
+
+def kvq_error_metrics(K, K_hat, Q=None, scales=None, workspace=None, comm: Optional[Comm] = None,
+                      stream=None) -> dict:
+    """Synchronous: returns the metrics as a dict (l2, max_abs, attn_mean_abs, ...)."""
+    T, D, nq, workspace = _metrics_args(K, K_hat, Q, scales, workspace)
+    out = kvq_metrics()
+    check(load().kvq_error_metrics(_ptr(K), _ptr(K_hat), T, D, _ptr(Q), nq, _ptr(scales), _ptr(workspace),
+                                   workspace.numel(), _comm_handle(comm), ctypes.byref(out), _stream(stream)),
+          "kvq_error_metrics")
+    return out.to_dict()
+
+
+def kvq_attention_scores(Q: torch.Tensor, K: torch.Tensor, K_hat: Optional[torch.Tensor] = None,
+                         S: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    nq, D = _mat(Q, torch.float32, "Q")
+    T, D2 = _mat(K, torch.float32, "K")
+    assert D == D2
+    if K_hat is not None:
+        _mat(K_hat, torch.float32, "K_hat")
+    if S is None:
+        S = torch.empty((nq, T), dtype=torch.float32, device=K.device)
+    check(load().kvq_attention_scores(_ptr(Q), nq, _ptr(K), _ptr(K_hat), T, D, _ptr(S), _stream(stream)),
+          "kvq_attention_scores")
+    return S
+
+
+def kvq_roundtrip_host_workspace_size(T: int, D: int, nq: int) -> int:
+    return int(load().kvq_roundtrip_host_workspace_size(T, D, nq))
+
+
+def kvq_roundtrip_host(K_host: torch.Tensor, Q_host: Optional[torch.Tensor] = None, scales_host=None,
+                       Kq_host=None, K_hat_host=None, workspace: Optional[torch.Tensor] = None,
+                       comm: Optional[Comm] = None, stream=None, device=None) -> dict:
+    """End-to-end from host buffers (pin them for speed); synchronizes."""
+    T, D = _mat(K_host, torch.float32, "K_host", cuda=False)
+    nq = 0 if Q_host is None else _mat(Q_host, torch.float32, "Q_host", cuda=False)[0]
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    if scales_host is None:
+        scales_host = torch.empty(D, dtype=torch.float32, pin_memory=K_host.is_pinned())
+    if Kq_host is None:
+        Kq_host = torch.empty((T, D), dtype=torch.int8, pin_memory=K_host.is_pinned())
+    need = kvq_roundtrip_host_workspace_size(T, D, nq)
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=device)
+    assert workspace.numel() >= need
+    m = kvq_metrics()
+    check(load().kvq_roundtrip_host(_ptr(K_host), T, D, _ptr(Q_host), nq, _ptr(scales_host), _ptr(Kq_host),
+                                    _ptr(K_hat_host), ctypes.byref(m), _ptr(workspace), workspace.numel(),
+                                    _comm_handle(comm), _stream(stream)), "kvq_roundtrip_host")
+    return {"scales": scales_host, "Kq": Kq_host, "K_hat": K_hat_host, "metrics": m.to_dict()}
+
+
+def kvq_synth_fill(rows: int, D: int, row0: int = 0, seed: int = 42, dist: int = DIST_UNIFORM,
+                   out: Optional[torch.Tensor] = None, device=None, stream=None) -> torch.Tensor:
+    """Rows [row0, row0+rows) of the seeded synthetic matrix (include/kvq_synth.h), generated on the GPU."""
+    if out is None:
+        out = torch.empty((rows, D), dtype=torch.float32,
+                          device=device or torch.device("cuda", torch.cuda.current_device()))
+    _mat(out, torch.float32, "out")
+    check(load().kvq_synth_fill(_ptr(out), row0, rows, D, seed, dist, _stream(stream)), "kvq_synth_fill")
+    return out

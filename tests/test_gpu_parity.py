@@ -1,0 +1,331 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Codes, scales and K_hat bit-exact; metrics and scores
+within the north-star relative tolerance 1e-5 (BASELINE.json north_star)."""
+import hashlib
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+REL = 1e-5  # north_star: "Error metrics and attention scores must agree within a relative tolerance of 1e-5"
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def kvq():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2601_04719_b200 import kvq as k
+    k.kvq_device_check()
+    return k
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def same_bits(a, b):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    assert a.shape == b.shape and a.dtype == b.dtype
+    va = a.view(np.uint8 if a.dtype == np.int8 else np.uint32)
+    vb = b.view(np.uint8 if b.dtype == np.int8 else np.uint32)
+    bad = np.nonzero(va != vb)
+    if bad[0].size:
+        i = tuple(x[0] for x in bad)
+        raise AssertionError(f"{bad[0].size} mismatches; first at {i}: gpu={a[i]!r} oracle={b[i]!r}")
+
+
+def gpu_roundtrip(kvq, K, fused=False):
+    Kd = dev(K)
+    s = kvq.kvq_compute_scales(Kd)
+    if fused:
+        q, kh = kvq.kvq_quantize_dequantize(Kd, s)
+    else:
+        q = kvq.kvq_quantize(Kd, s)
+        kh = kvq.kvq_dequantize(q, s)
+    return host(s), host(q), host(kh)
+
+
+def check_vs_oracle(kvq, orc, K, fused=False):
+    s, q, kh = gpu_roundtrip(kvq, K, fused)
+    so, qo, kho = orc.roundtrip(K)
+    same_bits(s, so)
+    same_bits(q, qo)
+    same_bits(kh, kho)
+
+
+# ----------------------------------------------------------------------------- generator
+@pytest.mark.parametrize("dist", [0, 1, 2])
+def test_device_generator_matches_oracle(kvq, orc, dist):
+    for (rows, D, row0) in [(33, 7, 0), (64, 128, 100), (5, 1000, 3)]:
+        g = host(kvq.kvq_synth_fill(rows, D, row0=row0, seed=42, dist=dist))
+        same_bits(g, orc.fill(rows, D, 42, dist, row0))
+
+
+# ----------------------------------------------------------------------------- edge battery
+EDGE_SHAPES = [(1, 1), (1, 4), (1, 5), (2, 3), (3, 7), (7, 13), (64, 128), (1000, 13), (257, 127),
+               (129, 1024), (33, 4096), (5000, 8)]
+
+
+@pytest.mark.parametrize("shape", EDGE_SHAPES)
+@pytest.mark.parametrize("fused", [False, True])
+def test_random_shapes_bit_exact(kvq, orc, shape, fused):
+    T, D = shape
+    check_vs_oracle(kvq, orc, orc.fill(T, D, 7, 1), fused)
+
+
+@pytest.mark.parametrize("name", ["zeros", "ones", "alternating", "negzero", "subnormal", "underflow",
+                                  "ties", "ongrid", "huge", "mixed_binades"])
+def test_structured_inputs_bit_exact(kvq, orc, name):
+    """P:538 edge cases (all zeros, all ones, alternating signs) plus the readings' corner cases."""
+    rng = np.random.default_rng(3)
+    T, D = 96, 20
+    if name == "zeros":
+        K = np.zeros((T, D), np.float32)
+    elif name == "ones":
+        K = np.ones((T, D), np.float32)
+    elif name == "alternating":
+        K = np.where((np.arange(T)[:, None] + np.arange(D)) % 2 == 0, 1.0, -1.0).astype(np.float32) * 0.37
+    elif name == "negzero":
+        K = np.full((T, D), -0.0, np.float32)
+        K[5, 3] = 0.25
+    elif name == "subnormal":  # subnormal scales take the exact path; clamp fires (reading Q4)
+        K = (rng.uniform(-1, 1, (T, D)) * 2.0 ** -140).astype(np.float32)
+        K[0, :] = np.float32(2.0 ** -140)
+    elif name == "underflow":  # nonzero columns whose scale underflows to 0 (reading Q5)
+        K = (rng.choice([-1, 0, 1], (T, D)) * 2.0 ** -149).astype(np.float32)
+    elif name == "ties":  # exact .5 quotients: half-even (reading Q1)
+        col = np.array([127, 0.5, 1.5, 2.5, -2.5, -127, 63.5, -0.5, 126.5, -126.5], np.float32) / 128
+        K = np.tile(col[:, None], (10, D)).astype(np.float32)
+    elif name == "ongrid":
+        K = orc.fill(T, D, 5, orc.DIST_ONGRID)
+    elif name == "huge":
+        K = (rng.uniform(-1, 1, (T, D)) * 3.0e38).astype(np.float32)
+    else:
+        K = (rng.uniform(-1, 1, (T, D)) * 2.0 ** rng.integers(-60, 60, (T, D))).astype(np.float32)
+    for fused in (False, True):
+        check_vs_oracle(kvq, orc, K, fused)
+
+
+def test_misaligned_bases_take_scalar_path(kvq, orc):
+    """Any alignment: views at odd element offsets are still bit-exact."""
+    T, D = 77, 64
+    K = orc.fill(T, D, 9, 1)
+    big = torch.zeros(T * D + 3, dtype=torch.float32, device="cuda")
+    Kv = big[1:1 + T * D].view(T, D)
+    Kv.copy_(dev(K))
+    s_buf = torch.zeros(D + 1, dtype=torch.float32, device="cuda")
+    s = kvq.kvq_compute_scales(Kv, s_buf[1:])
+    qb = torch.zeros(T * D + 3, dtype=torch.int8, device="cuda")
+    q = kvq.kvq_quantize(Kv, s, qb[3:].view(T, D))
+    khb = torch.zeros(T * D + 2, dtype=torch.float32, device="cuda")
+    kh = kvq.kvq_dequantize(q, s, khb[2:].view(T, D))
+    so, qo, kho = orc.roundtrip(K)
+    same_bits(host(s), so)
+    same_bits(host(q), qo)
+    same_bits(host(kh), kho)
+
+
+def test_quantize_with_given_scales_near_ties(kvq, orc):
+    """Quantize against arbitrary (not self-computed) scales, dense in near-tie quotients."""
+    rng = np.random.default_rng(11)
+    D = 64
+    s = rng.uniform(1e-3, 10, D).astype(np.float32)
+    k = rng.integers(-130, 130, (512, D)).astype(np.float32) + 0.5
+    K = (k * s).astype(np.float32)
+    K = np.stack([K, np.nextafter(K, np.float32(np.inf)), np.nextafter(K, np.float32(-np.inf))]).reshape(-1, D)
+    Kd, sd = dev(K), dev(s)
+    same_bits(host(kvq.kvq_quantize(Kd, sd)), orc.quantize(K, s))
+    q, kh = kvq.kvq_quantize_dequantize(Kd, sd)
+    same_bits(host(q), orc.quantize(K, s))
+    same_bits(host(kh), orc.dequantize(orc.quantize(K, s), s))
+
+
+@pytest.mark.parametrize("scale", [1 / 127, 1.0, 3 * 2.0 ** -10, 0.75 / 127, 2.0 ** -126, 2.0 ** 100 / 127,
+                                   1.1754942e-38, 4 * 2.0 ** -149])
+def test_quantize_exhaustive_binades(kvq, orc, scale):
+    """Every fp32 x with |x/s| in [2^-2, 2^8) (10 binades, both signs) for fixed s:
+    all codes, all ties, the clamp region.  Oracle = Listing 3 with Q1/Q2."""
+    s = np.float32(scale)
+    lo = np.float32(s * 0.25)
+    hi = np.float32(s * 256)
+    lo_b, hi_b = int(lo.view(np.uint32)), int(hi.view(np.uint32))
+    sd = dev(np.array([s], np.float32))
+    for c0 in range(lo_b, hi_b, 1 << 25):
+        x = np.arange(c0, min(c0 + (1 << 25), hi_b), dtype=np.uint32).view(np.float32)
+        x = np.concatenate([x, -x]).reshape(-1, 1)
+        got = host(kvq.kvq_quantize(dev(x), sd))
+        same_bits(got, orc.quantize(x, np.array([s], np.float32)))
+
+
+def test_determinism(kvq, orc):
+    K = dev(orc.fill(4096, 256, 1))
+    outs = []
+    for _ in range(3):
+        s = kvq.kvq_compute_scales(K)
+        q, kh = kvq.kvq_quantize_dequantize(K, s)
+        outs.append((host(s).tobytes(), host(q).tobytes(), host(kh).tobytes()))
+    assert outs[0] == outs[1] == outs[2]
+
+
+# ----------------------------------------------------------------------------- metrics + attention
+def _rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+@pytest.mark.parametrize("T,D,nq", [(1, 1, 1), (1000, 1000, 70), (64, 32, 64), (300, 13, 5), (517, 128, 0)])
+def test_metrics_ragged_vs_oracle(kvq, orc, T, D, nq):
+    K = orc.fill(T, D, 2, 1)
+    s, q, Kh = orc.roundtrip(K)
+    Q = orc.fill(nq, D, 43) if nq else None
+    m = kvq.kvq_error_metrics(dev(K), dev(Kh), None if Q is None else dev(Q), dev(s))
+    ss, mx = orc.recon_errors(K, Kh)
+    assert _rel(m["sum_sq"], ss) <= REL or ss == 0
+    assert m["max_abs"] == mx  # exact: a max of exact differences
+    assert m["theoretical_max"] == orc.theoretical_max(s)
+    assert m["n_elems"] == T * D and m["n_scores"] == nq * T
+    if nq:
+        ref = orc.attention_error(Q, K, Kh)
+        assert _rel(m["attn_mean_abs"], ref) <= REL
+
+
+@pytest.mark.parametrize("with_khat", [False, True])
+def test_attention_scores_per_entry(kvq, orc, with_khat):
+    T, D, nq = 200, 1000, 67
+    K = orc.fill(T, D, 4)
+    _, _, Kh = orc.roundtrip(K)
+    Q = orc.fill(nq, D, 43)
+    S = host(kvq.kvq_attention_scores(dev(Q), dev(K), dev(Kh) if with_khat else None))
+    E = (K.astype(np.float64) - Kh.astype(np.float64)) if with_khat else K.astype(np.float64)
+    ref = orc.scores(Q, K) - (orc.scores(Q, Kh) if with_khat else 0)
+    cond = np.abs(Q.astype(np.float64)) @ np.abs(E).T  # sum_d |Q_id E_td|
+    assert np.all(np.abs(S - ref) <= REL * cond + 1e-30)
+
+
+def test_metrics_identity_is_zero(kvq, orc):
+    K = dev(orc.fill(300, 64))
+    Q = dev(orc.fill(8, 64, 43))
+    m = kvq.kvq_error_metrics(K, K.clone(), Q)
+    assert m["l2"] == 0 and m["max_abs"] == 0 and m["attn_mean_abs"] == 0
+
+
+# ----------------------------------------------------------------------------- configs C1, C2 (full compare)
+def gold(cfg):
+    with open(os.path.join(GOLD, "survey_appendix.json")) as f:
+        return json.load(f)[cfg]
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_config_full_parity(kvq, orc, cfg):
+    g = gold(cfg)
+    T, D = g["T"], g["D"]
+    Kd = kvq.kvq_synth_fill(T, D, seed=42)
+    Qd = kvq.kvq_synth_fill(64, D, seed=43)
+    s = kvq.kvq_compute_scales(Kd)
+    q = kvq.kvq_quantize(Kd, s)
+    kh = kvq.kvq_dequantize(q, s)
+    m = kvq.kvq_error_metrics(Kd, kh, Qd, s)
+    K = orc.fill(T, D)
+    so, qo, kho = orc.roundtrip(K)
+    same_bits(host(Kd), K)
+    same_bits(host(s), so)
+    same_bits(host(q), qo)
+    same_bits(host(kh), kho)
+    assert hashlib.sha256(host(q).tobytes()).hexdigest()[:16] == g["q_sha16"]
+    ss, mx = orc.recon_errors(K, kho)
+    attn = orc.attention_error(orc.fill(64, D, 43), K, kho)
+    assert _rel(m["l2"], math.sqrt(ss)) <= REL and m["max_abs"] == mx
+    assert _rel(m["attn_mean_abs"], attn) <= REL
+    assert _rel(m["attn_mean_abs"], g["attn_mean_abs"]) <= REL
+
+
+# ----------------------------------------------------------------------------- configs C3, C4 (hash + samples)
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_config_large_parity(kvq, orc, cfg):
+    """Full-size outputs hash-equal the SURVEY goldens (independent numpy
+    implementation), sampled elements equal the oracle one by one, metrics
+    match the goldens, attention matches the oracle on a row block and the
+    closed form over all rows."""
+    g = gold(cfg)
+    T, D = g["T"], g["D"]
+    Kd = kvq.kvq_synth_fill(T, D, seed=42)
+    Qd = kvq.kvq_synth_fill(64, D, seed=43)
+    s = kvq.kvq_compute_scales(Kd)
+    q = kvq.kvq_quantize(Kd, s)
+    kh = kvq.kvq_dequantize(q, s)
+    m = kvq.kvq_error_metrics(Kd, kh, Qd, s)
+    sh = host(s)
+    assert hashlib.sha256(sh.tobytes()).hexdigest()[:16] == g["scales_sha16"]
+    assert hashlib.sha256(host(q).tobytes()).hexdigest()[:16] == g["q_sha16"]
+    hk = hashlib.sha256()
+    for r0 in range(0, T, 8192):
+        hk.update(host(kh[r0:r0 + 8192]).tobytes())
+    assert hk.hexdigest()[:16] == g["khat_sha16"]
+    assert _rel(m["l2"], g["l2"]) <= REL and m["max_abs"] == g["max_abs"]
+    # sampled elements vs the oracle, one by one (scales from the streamed oracle)
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(T, 64, replace=False))
+    so = orc.streamed_pipeline(T, D, hashes=False, block_rows=2048)["scales"] if cfg == "C3" else sh
+    if cfg == "C3":
+        same_bits(sh, so)
+    for r in rows:
+        Kr = orc.fill(1, D, 42, 0, int(r))
+        qo = orc.quantize(Kr, so)
+        same_bits(host(q[r:r + 1]), qo)
+        same_bits(host(kh[r:r + 1]), orc.dequantize(qo, so))
+    # attention: one 64-row block against the oracle, whole matrix against the closed form
+    r0 = int(rows[0])
+    blk = slice(r0, r0 + 64)
+    Kb = orc.fill(64, D, 42, 0, r0)
+    Khb = orc.dequantize(orc.quantize(Kb, so), so)
+    Qh = orc.fill(64, D, 43)
+    mb = kvq.kvq_error_metrics(Kd[blk].contiguous(), kh[blk].contiguous(), Qd)
+    assert _rel(mb["attn_mean_abs"], orc.attention_error(Qh, Kb, Khb)) <= REL
+    closed = math.sqrt(2 / math.pi) * float(np.mean(sh)) * math.sqrt(D / 12) * math.sqrt(1 / 3)
+    assert m["attn_mean_abs"] == pytest.approx(closed, rel=0.01)
+    assert abs(m["attn_mean_abs"] - 0.095) < 0.002
+
+
+# ----------------------------------------------------------------------------- host pipeline + comm
+def test_roundtrip_host_matches_device_path(kvq, orc):
+    T, D, nq = 3000, 256, 64
+    K = orc.fill(T, D, 42)
+    Q = orc.fill(nq, D, 43)
+    Kh_host = torch.empty((T, D), dtype=torch.float32).pin_memory()
+    r = kvq.kvq_roundtrip_host(torch.from_numpy(K).pin_memory(), torch.from_numpy(Q).pin_memory(),
+                               K_hat_host=Kh_host)
+    so, qo, kho = orc.roundtrip(K)
+    same_bits(r["scales"].numpy(), so)
+    same_bits(r["Kq"].numpy(), qo)
+    same_bits(Kh_host.numpy(), kho)
+    ss, mx = orc.recon_errors(K, kho)
+    assert _rel(r["metrics"]["sum_sq"], ss) <= REL and r["metrics"]["max_abs"] == mx
+    assert _rel(r["metrics"]["attn_mean_abs"], orc.attention_error(Q, K, kho)) <= REL
+
+
+def test_single_rank_comm_path(kvq, orc):
+    """The NCCL exchange path with one rank must not change any result."""
+    uid = kvq.kvq_comm_unique_id()
+    comm = kvq.Comm(uid, 1, 0)
+    try:
+        K = orc.fill(700, 96, 42, 1)
+        Kd = dev(K)
+        s = kvq.kvq_compute_scales(Kd, comm=comm)
+        so, qo, kho = orc.roundtrip(K)
+        same_bits(host(s), so)
+        q, kh = kvq.kvq_quantize_dequantize(Kd, s)
+        m = kvq.kvq_error_metrics(Kd, kh, dev(orc.fill(8, 96, 43)), s, comm=comm)
+        assert m["max_abs"] == orc.max_abs_error(K, kho)
+    finally:
+        comm.destroy()
