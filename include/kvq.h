@@ -115,7 +115,9 @@ kvq_status kvq_quantize_dequantize(const float *K, const float *scales, int64_t 
  * out_dev: DEVICE pointer to one kvq_metrics, written asynchronously.
  * comm != NULL: K/K_hat are this rank's token shard; sums and maxima are
  * all-reduced so every rank receives the global metrics.
- * Accumulation is fp64 with a fixed reduction tree (deterministic). */
+ * a6 runs on the tcgen05 tensor cores (3xTF32) when 1 <= nq <= 64, D % 4 == 0
+ * and K/K_hat are 16-byte aligned, else on the CUDA cores.  Sums are carried in
+ * fp64 and reduced with a fixed tree (deterministic run to run). */
 size_t kvq_error_metrics_workspace_size(int64_t T, int64_t D, int64_t nq);
 kvq_status kvq_error_metrics_async(const float *K, const float *K_hat, int64_t T, int64_t D,
                                    const float *Q, int64_t nq, const float *scales,
@@ -130,10 +132,16 @@ kvq_status kvq_error_metrics(const float *K, const float *K_hat, int64_t T, int6
 /* Raw attention scores for parity checks of a6 (reading Q10):
  *   K_hat == NULL:  S[i][t] = sum_d Q[i][d] * K[t][d]
  *   K_hat != NULL:  S[i][t] = sum_d Q[i][d] * (K[t][d] - K_hat[t][d])   (= S - S')
- * Q: [nq][D], K/K_hat: [T][D], S: [nq][T] float32 out; fp32 products with
- * per-32-term fp32 partial sums carried in fp64. */
+ * Q: [nq][D], K/K_hat: [T][D], S: [nq][T] float32 out.
+ * With a workspace of kvq_attention_scores_workspace_size(D, nq) bytes, nq <= 64,
+ * D % 4 == 0 and 16-byte aligned K/K_hat the contraction runs on the tcgen05
+ * tensor cores (3xTF32 split, fp32 accumulation in TMEM); otherwise (or with
+ * workspace == NULL) on the CUDA cores (fp32 products, 32-term fp32 partial
+ * sums carried in fp64).  Both are GPU paths. */
+size_t kvq_attention_scores_workspace_size(int64_t D, int64_t nq);
 kvq_status kvq_attention_scores(const float *Q, int64_t nq, const float *K, const float *K_hat,
-                                int64_t T, int64_t D, float *S, void *stream);
+                                int64_t T, int64_t D, float *S, void *workspace, size_t workspace_bytes,
+                                void *stream);
 
 /* ---------------------------------------------------------------- host-buffer pipeline */
 /* The whole path from HOST memory (the end-to-end call a user makes):

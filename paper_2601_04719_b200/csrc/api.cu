@@ -223,12 +223,18 @@ extern "C" kvq_status kvq_error_metrics(const float *K, const float *K_hat, int6
     return cuda_check(cudaStreamSynchronize(s), "sync metrics");
 }
 
+extern "C" size_t kvq_attention_scores_workspace_size(int64_t D, int64_t nq) {
+    if (D < 1 || nq < 1) return 0;
+    return attention_scores_workspace_size(D, nq);
+}
+
 extern "C" kvq_status kvq_attention_scores(const float *Q, int64_t nq, const float *K, const float *K_hat, int64_t T,
-                                           int64_t D, float *S, void *stream) {
+                                           int64_t D, float *S, void *workspace, size_t workspace_bytes,
+                                           void *stream) {
     KVQ_REQUIRE(Q && K && S, "kvq_attention_scores: NULL pointer");
     KVQ_REQUIRE(!bad_dims(T, D) && nq >= 1 && nq <= (int64_t(1) << 62) / T, "kvq_attention_scores: bad sizes");
     KVQ_TRY(device_ok());
-    return launch_attention_scores(Q, nq, K, K_hat, T, D, S, (cudaStream_t)stream);
+    return launch_attention_scores(Q, nq, K, K_hat, T, D, S, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 // ------------------------------------------------------------------------------ host-buffer pipeline

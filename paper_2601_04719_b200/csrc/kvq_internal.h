@@ -43,7 +43,16 @@ kvq_status launch_quantize(const float *K, const float *scales, int64_t T, int64
 kvq_status launch_dequantize(const int8_t *Kq, const float *scales, int64_t T, int64_t D, float *K_hat,
                              cudaStream_t s);
 
-// ---- metrics kernels (metrics_kernels.cu)
+// ---- metrics kernels (metrics_kernels.cu, attn_tc.cu)
+struct Partial {  // per-CTA partial sums of a5/a6
+    double sum_sq, attn_abs, max_abs, pad;
+};
+bool tc_eligible(const float *K, const float *K_hat, int64_t T, int64_t D, int64_t nq);
+size_t tc_qsplit_bytes(int64_t D);
+// mode 0: write per-CTA Partials (grid returned in *grid_out); mode 1: write S [nq][T].
+kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
+                          int64_t nq, void *ws_q, void *partials, int *grid_out, float *S, cudaStream_t s);
+bool force_simt();  // KVQ_FORCE_SIMT=1: use the CUDA-core attention kernel (tests compare the two)
 size_t metrics_workspace_size(int64_t T, int64_t D, int64_t nq);
 // Writes per-rank totals {sum_sq, attn_abs_sum, n_elems, n_scores} (double[4]) and
 // {max_abs_bits, theo_max_bits} (uint64[2]) into the workspace tail; returns
@@ -56,8 +65,9 @@ kvq_status launch_metrics_partials(const float *K, const float *K_hat, int64_t T
                                    int64_t nq, const float *scales, void *ws, size_t ws_bytes,
                                    MetricTotals *totals, cudaStream_t s);
 kvq_status launch_metrics_finalize(const MetricTotals &totals, kvq_metrics *out_dev, cudaStream_t s);
+size_t attention_scores_workspace_size(int64_t D, int64_t nq);
 kvq_status launch_attention_scores(const float *Q, int64_t nq, const float *K, const float *K_hat, int64_t T,
-                                   int64_t D, float *S, cudaStream_t s);
+                                   int64_t D, float *S, void *ws, size_t ws_bytes, cudaStream_t s);
 
 // ---- comm (comm.cpp)
 kvq_status comm_allreduce_max_u32(kvq_comm_t comm, uint32_t *buf, size_t count, cudaStream_t s);

@@ -12,6 +12,7 @@
 // ~32 u sum|Q E| instead of D u sum|Q E|.  Per-CTA partials are reduced by a
 // single CTA in a fixed order: metrics are deterministic run to run.
 #include <algorithm>
+#include <cstdlib>
 
 #include "device_common.cuh"
 #include "kvq_internal.h"
@@ -19,13 +20,6 @@
 namespace kvq {
 
 constexpr int kTileRows = 64, kTileQ = 64, kChunk = 32, kPad = 68;
-
-struct Partial {
-    double sum_sq;
-    double attn_abs;
-    double max_abs;
-    double pad;
-};
 
 // MODE 0: metrics partials (E = K - K_hat).  MODE 1: write S (E = K or K - K_hat) to `S`.
 template <int MODE>
@@ -231,10 +225,18 @@ __global__ void metrics_finalize_kernel(const double *sums, const uint64_t *maxe
 // ---------------------------------------------------------------------------- host side
 static int64_t num_tiles(int64_t T) { return (T + kTileRows - 1) / kTileRows; }
 
+bool force_simt() {
+    const char *e = std::getenv("KVQ_FORCE_SIMT");
+    return e && e[0] == '1';
+}
+
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// workspace: [partials (max(simt tiles, 1024 CTAs)) | Q split tiles | totals]
 size_t metrics_workspace_size(int64_t T, int64_t D, int64_t nq) {
-    (void)D;
     (void)nq;
-    return (size_t)num_tiles(T) * sizeof(Partial) + 4 * sizeof(double) + 2 * sizeof(uint64_t) + 256;
+    const size_t np = (size_t)std::max<int64_t>(num_tiles(T), 1024);
+    return 256 + al256(np * sizeof(Partial)) + al256(tc_qsplit_bytes(D)) + 4 * sizeof(double) + 2 * sizeof(uint64_t);
 }
 
 kvq_status launch_metrics_partials(const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
@@ -244,12 +246,23 @@ kvq_status launch_metrics_partials(const float *K, const float *K_hat, int64_t T
         return fail(KVQ_ERR_INVALID_VALUE, "error_metrics: workspace too small");
     uintptr_t base = (reinterpret_cast<uintptr_t>(ws) + 255) & ~(uintptr_t)255;
     Partial *partials = reinterpret_cast<Partial *>(base);
-    const int64_t nt = num_tiles(T);
-    totals->sums = reinterpret_cast<double *>(partials + nt);
+    const size_t np = (size_t)std::max<int64_t>(num_tiles(T), 1024);
+    void *qsplit = reinterpret_cast<void *>(base + al256(np * sizeof(Partial)));
+    totals->sums = reinterpret_cast<double *>(base + al256(np * sizeof(Partial)) + al256(tc_qsplit_bytes(D)));
     totals->maxes = reinterpret_cast<uint64_t *>(totals->sums + 4);
-    attn_tile_kernel<0><<<(unsigned)nt, 256, 0, s>>>(K, K_hat, Q, T, D, nq, partials, nullptr);
-    if (kvq_status st = check_launch("metrics_tiles"); st != KVQ_OK) return st;
-    reduce_partials_kernel<<<1, 1024, 0, s>>>(partials, nt, scales, D, (double)T * (double)D,
+    int64_t nparts;
+    if (!force_simt() && tc_eligible(K, K_hat, T, D, nq)) {
+        int grid = 0;
+        if (kvq_status st = launch_attn_tc(0, K, K_hat, T, D, Q, nq, qsplit, partials, &grid, nullptr, s);
+            st != KVQ_OK)
+            return st;
+        nparts = grid;
+    } else {
+        nparts = num_tiles(T);
+        attn_tile_kernel<0><<<(unsigned)nparts, 256, 0, s>>>(K, K_hat, Q, T, D, nq, partials, nullptr);
+        if (kvq_status st = check_launch("metrics_tiles"); st != KVQ_OK) return st;
+    }
+    reduce_partials_kernel<<<1, 1024, 0, s>>>(partials, nparts, scales, D, (double)T * (double)D,
                                               (double)nq * (double)T, totals->sums, totals->maxes);
     return check_launch("metrics_reduce");
 }
@@ -259,8 +272,19 @@ kvq_status launch_metrics_finalize(const MetricTotals &t, kvq_metrics *out_dev, 
     return check_launch("metrics_finalize");
 }
 
+size_t attention_scores_workspace_size(int64_t D, int64_t nq) {
+    (void)nq;
+    return tc_qsplit_bytes(D) + 256;
+}
+
 kvq_status launch_attention_scores(const float *Q, int64_t nq, const float *K, const float *K_hat, int64_t T,
-                                   int64_t D, float *S, cudaStream_t s) {
+                                   int64_t D, float *S, void *ws, size_t ws_bytes, cudaStream_t s) {
+    const bool tc = ws && ws_bytes >= attention_scores_workspace_size(D, nq) && !force_simt() &&
+                    tc_eligible(K, K_hat ? K_hat : K, T, D, nq);
+    if (tc) {
+        void *qsplit = reinterpret_cast<void *>((reinterpret_cast<uintptr_t>(ws) + 255) & ~(uintptr_t)255);
+        return launch_attn_tc(1, K, K_hat, T, D, Q, nq, qsplit, nullptr, nullptr, S, s);
+    }
     attn_tile_kernel<1><<<(unsigned)num_tiles(T), 256, 0, s>>>(K, K_hat, Q, T, D, nq, nullptr, S);
     return check_launch("attention_scores");
 }

@@ -186,7 +186,8 @@ def kvq_error_metrics(K, K_hat, Q=None, scales=None, workspace=None, comm: Optio
 
 
 def kvq_attention_scores(Q: torch.Tensor, K: torch.Tensor, K_hat: Optional[torch.Tensor] = None,
-                         S: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+                         S: Optional[torch.Tensor] = None, workspace="auto", stream=None) -> torch.Tensor:
+    """workspace="auto" allocates the tensor-core workspace; None selects the CUDA-core kernel."""
     nq, D = _mat(Q, torch.float32, "Q")
     T, D2 = _mat(K, torch.float32, "K")
     assert D == D2
@@ -194,8 +195,12 @@ def kvq_attention_scores(Q: torch.Tensor, K: torch.Tensor, K_hat: Optional[torch
         _mat(K_hat, torch.float32, "K_hat")
     if S is None:
         S = torch.empty((nq, T), dtype=torch.float32, device=K.device)
-    check(load().kvq_attention_scores(_ptr(Q), nq, _ptr(K), _ptr(K_hat), T, D, _ptr(S), _stream(stream)),
-          "kvq_attention_scores")
+    if isinstance(workspace, str):
+        workspace = torch.empty(int(load().kvq_attention_scores_workspace_size(D, nq)), dtype=torch.uint8,
+                                device=K.device)
+    nbytes = 0 if workspace is None else workspace.numel()
+    check(load().kvq_attention_scores(_ptr(Q), nq, _ptr(K), _ptr(K_hat), T, D, _ptr(S), _ptr(workspace), nbytes,
+                                      _stream(stream)), "kvq_attention_scores")
     return S
 
 

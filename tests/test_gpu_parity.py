@@ -329,3 +329,58 @@ def test_single_rank_comm_path(kvq, orc):
         assert m["max_abs"] == orc.max_abs_error(K, kho)
     finally:
         comm.destroy()
+
+
+# ----------------------------------------------------------------------------- tensor-core (tcgen05) attention path
+TC_CASES = [(1, 4, 1), (128, 32, 64), (129, 36, 64), (1000, 1000, 64), (300, 128, 17), (257, 8192, 64),
+            (4096, 1024, 64), (64, 4, 3)]
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("T,D,nq", TC_CASES)
+def test_tc_metrics_vs_oracle(kvq, orc, T, D, nq):
+    """a5 + a6 on tcgen05 (3xTF32, TMEM accumulation): ragged T (not a multiple of
+    128), ragged D (not a multiple of 32), nq < 64, against the fp64 oracle."""
+    K = orc.fill(T, D, 2, 1)
+    s, q, Kh = orc.roundtrip(K)
+    Q = orc.fill(nq, D, 43)
+    m = kvq.kvq_error_metrics(dev(K), dev(Kh), dev(Q), dev(s))
+    ss, mx = orc.recon_errors(K, Kh)
+    assert _rel(m["sum_sq"], ss) <= REL
+    assert m["max_abs"] == mx
+    assert m["n_elems"] == T * D and m["n_scores"] == nq * T
+    assert _rel(m["attn_mean_abs"], orc.attention_error(Q, K, Kh)) <= REL
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("T,D,nq", [(200, 1000, 64), (333, 8192, 64), (130, 36, 5), (64, 128, 64)])
+@pytest.mark.parametrize("with_khat", [False, True])
+@pytest.mark.parametrize("path", ["tc", "simt"])
+def test_scores_per_entry_both_paths(kvq, orc, T, D, nq, with_khat, path):
+    K = orc.fill(T, D, 4)
+    _, _, Kh = orc.roundtrip(K)
+    Q = orc.fill(nq, D, 43)
+    S = host(kvq.kvq_attention_scores(dev(Q), dev(K), dev(Kh) if with_khat else None,
+                                      workspace="auto" if path == "tc" else None))
+    E = (K.astype(np.float64) - Kh.astype(np.float64)) if with_khat else K.astype(np.float64)
+    ref = orc.scores(Q, K) - (orc.scores(Q, Kh) if with_khat else 0)
+    cond = np.abs(Q.astype(np.float64)) @ np.abs(E).T
+    err = np.abs(S - ref) / np.maximum(cond, 1e-300)
+    assert err.max() <= REL, (path, float(err.max()))
+
+
+@pytest.mark.timeout(300)
+def test_tc_and_simt_metrics_agree(kvq, orc, monkeypatch):
+    T, D, nq = 2048, 2048, 64
+    Kd = kvq.kvq_synth_fill(T, D, seed=42)
+    Qd = kvq.kvq_synth_fill(nq, D, seed=43)
+    s = kvq.kvq_compute_scales(Kd)
+    q, kh = kvq.kvq_quantize_dequantize(Kd, s)
+    m_tc = kvq.kvq_error_metrics(Kd, kh, Qd, s)
+    monkeypatch.setenv("KVQ_FORCE_SIMT", "1")
+    m_simt = kvq.kvq_error_metrics(Kd, kh, Qd, s)
+    assert m_tc["max_abs"] == m_simt["max_abs"]
+    assert _rel(m_tc["sum_sq"], m_simt["sum_sq"]) <= 1e-12
+    assert _rel(m_tc["attn_mean_abs"], m_simt["attn_mean_abs"]) <= REL
+    # deterministic run to run
+    assert kvq.kvq_error_metrics(Kd, kh, Qd, s) == kvq.kvq_error_metrics(Kd, kh, Qd, s)
