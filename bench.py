@@ -35,7 +35,7 @@ CONFIGS = {  # BASELINE.json configs
 }
 METRIC = "quantize+dequantize elements/s and achieved HBM GB/s vs B200 peak at 1/2/4/8 GPUs"
 # Algorithmic bytes per element of each pass: what the method itself must move.
-BYTES = {"scales": 4, "quantize": 5, "dequantize": 5, "metrics": 8}
+BYTES = {"scales": 4, "quantize": 5, "dequantize": 5, "metrics": 8, "roundtrip": 9}
 
 
 def peaks():
@@ -176,10 +176,11 @@ def run_kvq(args, cfg, rank, world, local_rank):
     scales = torch.empty(D, dtype=torch.float32, device=dev)
     Kq = torch.empty((rows, D), dtype=torch.int8, device=dev)
     Kh = torch.empty((rows, D), dtype=torch.float32, device=dev)
-    ws = torch.empty(kvq.kvq_error_metrics_workspace_size(rows, D, nq), dtype=torch.uint8, device=dev)
+    ws = torch.empty(kvq.kvq_roundtrip_workspace_size(rows, D, nq), dtype=torch.uint8, device=dev)
     mout = torch.empty(kvq.METRICS_BYTES, dtype=torch.uint8, device=dev)
 
-    def step(ev=None):
+    def step_separate(ev=None):
+        """The four separate ABI calls (a1+a2+a7, a3, a4, a5+a6): 22 B/elem."""
         if ev is not None:
             ev[0].record(stream)
         kvq.kvq_compute_scales(K, scales, comm=comm, stream=stream)
@@ -194,6 +195,21 @@ def run_kvq(args, cfg, rank, world, local_rank):
         kvq.kvq_error_metrics_async(K, Kh, Q, scales, out_dev=mout, workspace=ws, comm=comm, stream=stream)
         if ev is not None:
             ev[4].record(stream)
+
+    def step_fused(ev=None):
+        """kvq_compute_scales (a1+a2+a7) then kvq_roundtrip (a3+a4+a5+a6 in one pass): 13 B/elem."""
+        if ev is not None:
+            ev[0].record(stream)
+        kvq.kvq_compute_scales(K, scales, comm=comm, stream=stream)
+        if ev is not None:
+            ev[1].record(stream)
+        kvq.kvq_roundtrip(K, scales, Q, Kq, Kh, out_dev=mout, workspace=ws, comm=comm, stream=stream)
+        if ev is not None:
+            ev[2].record(stream)
+
+    step = step_fused if args.pipeline == "fused" else step_separate
+    pass_names = ["scales", "roundtrip"] if args.pipeline == "fused" else ["scales", "quantize", "dequantize",
+                                                                            "metrics"]
 
     for _ in range(args.warmup):
         step()
@@ -220,8 +236,7 @@ def run_kvq(args, cfg, rank, world, local_rank):
     # per-pass device time (events on the launching stream), averaged over the timed steps
     passes = {}
     if args.pass_events:
-        names = ["scales", "quantize", "dequantize", "metrics"]
-        for j, nme in enumerate(names):
+        for j, nme in enumerate(pass_names):
             passes[nme] = statistics.mean(e[j].elapsed_time(e[j + 1]) for e in evs)
     n_local = rows * D
     pk = peaks()
@@ -266,7 +281,8 @@ def run_kvq(args, cfg, rank, world, local_rank):
     if rank != 0:
         return
     value = T * D / (ms * 1e-3)
-    algo_bytes = sum(BYTES.values()) * T * D
+    algo_per_elem = sum(BYTES[n] for n in pass_names)
+    algo_bytes = algo_per_elem * T * D
     roofline = None
     if dom:
         t = passes[dom]
@@ -287,14 +303,17 @@ def run_kvq(args, cfg, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (splitmix64 lattice uniform [-1,1), SURVEY §8(d))",
         "config": {"workload": f"{cfg['name']}: {cfg['desc']}", "T": T, "D": D, "nq": nq,
-                   "step": "compute_scales(+allreduce MAX) -> quantize -> dequantize -> error_metrics(L2,max,attn)",
+                   "step": ("kvq_compute_scales(a1,a2,+a7 allreduce MAX) -> kvq_roundtrip(a3 quantize, a4 dequantize,"
+                            " a5 L2/max, a6 attention error; one HBM pass)") if args.pipeline == "fused" else
+                           "kvq_compute_scales -> kvq_quantize -> kvq_dequantize -> kvq_error_metrics_async",
+                   "pipeline": args.pipeline,
                    "l2_flush": "none needed: inputs larger than L2 (K alone is %.2f GB > 126 MB)" % (4 * T * D / 1e9)
                    if 4 * T * D > 2 * 126e6 else "inputs L2-resident (warm)",
                    "parallelism": f"token-shard x{world}"},
-        "hbm": {"GBps": algo_bytes / (ms * 1e-3) / 1e9 / world, "algo_bytes_per_elem": sum(BYTES.values()),
+        "hbm": {"GBps": algo_bytes / (ms * 1e-3) / 1e9 / world, "algo_bytes_per_elem": algo_per_elem,
                 "frac_of_peak_per_gpu": algo_bytes / (ms * 1e-3) / 1e9 / world / pk["hbm_gbs"]},
         "passes": pass_report, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": 7 * args.steps, "clocks": clk.summary(wall0, wall1),
+        "gpu_launches": (7 if args.pipeline == "fused" else 8) * args.steps, "clocks": clk.summary(wall0, wall1),
         "fidelity": {k: metrics[k] for k in ("l2", "max_abs", "attn_mean_abs", "theoretical_max")},
     }
     print(json.dumps(line), flush=True)
@@ -307,6 +326,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="kvq", choices=["kvq", "reference"])
+    ap.add_argument("--pipeline", default="fused", choices=["fused", "separate"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)

@@ -129,6 +129,22 @@ kvq_status kvq_error_metrics(const float *K, const float *K_hat, int64_t T, int6
                              void *workspace, size_t workspace_bytes, kvq_comm_t comm,
                              kvq_metrics *out_host, void *stream);
 
+/* a3+a4+a5+a6 in ONE pass over K (the B200 single-pass path; 9 B/elem of HBM
+ * traffic instead of 5 + 5 + 8): quantize (Eq. 7) and dequantize (Eq. 8) each
+ * K tile while it is on chip, write Kq and K_hat, and contract E = K - K_hat
+ * with Q on the tensor cores for the fidelity checks.  Kq and K_hat are
+ * bit-identical to kvq_quantize + kvq_dequantize; the metrics equal
+ * kvq_error_metrics on (K, K_hat) within 1e-5 (fp64 sums in another order).
+ * Single pass when 1 <= nq <= 64, D % 16 == 0 and K, Kq, K_hat are 16-byte
+ * aligned; otherwise the same results from the separate kernels.
+ * scales: [D] from kvq_compute_scales.  out_dev: DEVICE kvq_metrics, async.
+ * workspace: kvq_roundtrip_workspace_size(T, D, nq) bytes.  comm as in
+ * kvq_error_metrics_async. */
+size_t kvq_roundtrip_workspace_size(int64_t T, int64_t D, int64_t nq);
+kvq_status kvq_roundtrip(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
+                         float *K_hat, const float *Q, int64_t nq, void *workspace,
+                         size_t workspace_bytes, kvq_comm_t comm, kvq_metrics *out_dev, void *stream);
+
 /* Raw attention scores for parity checks of a6 (reading Q10):
  *   K_hat == NULL:  S[i][t] = sum_d Q[i][d] * K[t][d]
  *   K_hat != NULL:  S[i][t] = sum_d Q[i][d] * (K[t][d] - K_hat[t][d])   (= S - S')

@@ -223,6 +223,34 @@ extern "C" kvq_status kvq_error_metrics(const float *K, const float *K_hat, int6
     return cuda_check(cudaStreamSynchronize(s), "sync metrics");
 }
 
+extern "C" size_t kvq_roundtrip_workspace_size(int64_t T, int64_t D, int64_t nq) {
+    return kvq_error_metrics_workspace_size(T, D, nq);
+}
+
+extern "C" kvq_status kvq_roundtrip(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
+                                    float *K_hat, const float *Q, int64_t nq, void *workspace, size_t workspace_bytes,
+                                    kvq_comm_t comm, kvq_metrics *out_dev, void *stream) {
+    KVQ_REQUIRE(K && scales && Kq && K_hat && workspace && out_dev, "kvq_roundtrip: NULL pointer");
+    KVQ_REQUIRE(!bad_dims(T, D), "kvq_roundtrip: need T >= 1, D >= 1, T*D <= 2^62");
+    KVQ_REQUIRE(nq >= 0 && (nq == 0 || Q), "kvq_roundtrip: need nq >= 0 and Q when nq > 0");
+    KVQ_REQUIRE(nq <= (int64_t(1) << 62) / D && nq <= (int64_t(1) << 62) / T, "kvq_roundtrip: nq too large");
+    const size_t n = (size_t)(T * D);
+    KVQ_REQUIRE(!overlap(K, n * 4, Kq, n) && !overlap(K_hat, n * 4, K, n * 4) && !overlap(K_hat, n * 4, Kq, n) &&
+                    !overlap(scales, (size_t)D * 4, Kq, n) && !overlap(scales, (size_t)D * 4, K_hat, n * 4),
+                "kvq_roundtrip: outputs alias inputs");
+    KVQ_REQUIRE(workspace_bytes >= metrics_workspace_size(T, D, nq), "kvq_roundtrip: workspace too small");
+    KVQ_TRY(device_ok());
+    cudaStream_t s = (cudaStream_t)stream;
+    MetricTotals tot;
+    KVQ_TRY(launch_roundtrip_partials(K, scales, T, D, Kq, K_hat, nq ? Q : nullptr, nq, workspace, workspace_bytes,
+                                      &tot, s));
+    if (comm) {
+        KVQ_TRY(comm_allreduce_sum_f64(comm, tot.sums, 4, s));
+        KVQ_TRY(comm_allreduce_max_u64(comm, tot.maxes, 2, s));
+    }
+    return launch_metrics_finalize(tot, out_dev, s);
+}
+
 extern "C" size_t kvq_attention_scores_workspace_size(int64_t D, int64_t nq) {
     if (D < 1 || nq < 1) return 0;
     return attention_scores_workspace_size(D, nq);
@@ -321,7 +349,10 @@ extern "C" kvq_status kvq_roundtrip_host(const float *K_host, int64_t T, int64_t
         }
         if (comm && (st = comm_allreduce_max_u32(comm, bits, (size_t)D, s)) != KVQ_OK) break;
         if ((st = launch_finalize(bits, D, s)) != KVQ_OK) break;
-        if ((st = launch_quantize(K, sc, T, D, Kq, Kh, s)) != KVQ_OK) break;
+        MetricTotals tot;
+        if ((st = launch_roundtrip_partials(K, sc, T, D, Kq, Kh, nq ? Q : nullptr, nq, base + L.mws,
+                                            metrics_workspace_size(T, D, nq), &tot, s)) != KVQ_OK)
+            break;
         // codes + scales (+ K_hat) go back on the copy engine while the metrics run on `s`
         if ((st = cuda_check(cudaEventRecord(ev[nblk + 1], s), "record")) != KVQ_OK) break;
         if ((st = cuda_check(cudaStreamWaitEvent(cs, ev[nblk + 1], 0), "wait")) != KVQ_OK) break;
@@ -334,10 +365,6 @@ extern "C" kvq_status kvq_roundtrip_host(const float *K_host, int64_t T, int64_t
         if (K_hat_host && (st = cuda_check(cudaMemcpyAsync(K_hat_host, Kh, (size_t)(T * D) * 4,
                                                            cudaMemcpyDeviceToHost, cs),
                                            "D2H K_hat")) != KVQ_OK)
-            break;
-        MetricTotals tot;
-        if ((st = launch_metrics_partials(K, Kh, T, D, nq ? Q : nullptr, nq, sc, base + L.mws,
-                                          metrics_workspace_size(T, D, nq), &tot, s)) != KVQ_OK)
             break;
         if (comm) {
             if ((st = comm_allreduce_sum_f64(comm, tot.sums, 4, s)) != KVQ_OK) break;

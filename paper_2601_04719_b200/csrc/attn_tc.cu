@@ -1,32 +1,36 @@
-// attn_tc.cu — a5 + a6 on the 5th-generation tensor cores (tcgen05, TMEM, TMA).
+// attn_tc.cu — a5 + a6 (and the single-pass a3+a4+a5+a6) on the 5th-generation
+// tensor cores (tcgen05, TMEM, TMA).
 //
 // The attention-score error is a real dense contraction:
 //     Delta[t][i] = sum_d E[t][d] * Q[i][d],   E = K - K_hat   (exact in fp32)
-// with M = tokens, N = nq = 64 queries, K = D.  It runs on tcgen05 with fp32
+// with M = tokens, N = nq <= 64 queries, K = D.  It runs on tcgen05 with fp32
 // accuracy via the 3xTF32 split: E = E_hi + E_lo, Q = Q_hi + Q_lo (each part
 // rounded to tf32), Delta = E_hi Q_hi + E_hi Q_lo + E_lo Q_hi (the dropped
 // E_lo Q_lo term is ~2^-22 relative), accumulated in fp32 in TMEM.
 //
 // One persistent CTA per SM walks 128-row tiles; per 32-column K-block:
-//   warp 0 (1 lane)  TMA: K and K_hat boxes [128 x 32] fp32 (128B swizzle) into a
-//                    4-stage ring; 1-D bulk copy of the pre-split Q tile (hi+lo,
+//   warp 0 (1 lane)  TMA: K (and K_hat) boxes [128 x 32] fp32 (128B swizzle) and,
+//                    in the fused mode, the 32 per-column quantizer constants into
+//                    a 4-stage ring; 1-D bulk copy of the pre-split Q tile (hi+lo,
 //                    16 KB, already in the canonical UMMA layout) into a 4-stage ring.
-//   warps 2..5       converters, one token row per thread: read K/K_hat row
-//                    segments from smem, E = K - K_hat, accumulate sum E^2 (fp64)
-//                    and max |E| (a5), split E into tf32 hi/lo and tcgen05.st them
-//                    into a 2-stage A ring in TMEM (A operand read from TMEM: no
-//                    smem bandwidth for the 3 reads of E).
+//   warps 4..11      converters, one token row and 16 columns per thread (ld.shared):
+//                    [fused mode: quantize (Eq. 7) + dequantize (Eq. 8) the row
+//                    segment, stage codes and K_hat in swizzled smem and write them
+//                    with TMA bulk tensor stores (full 128-byte lines: no DRAM
+//                    read-modify-write for the 32-byte code segments)]
+//                    E = K - K_hat, sum E^2 and max |E| (a5), split E into tf32
+//                    hi/lo and tcgen05.st them into a 2-stage A ring in TMEM (the A
+//                    operand is read from TMEM: no smem bandwidth for E's 3 reads).
 //   warp 1 (1 lane)  issues 3 x 4 tcgen05.mma (M=128, N=64, K=8) per K-block into a
 //                    double-buffered TMEM accumulator, restarted every CHUNK_KB
 //                    K-blocks, and commits to the barriers.
-//   warps 6..9       epilogue, one row per thread: tcgen05.ld each finished
+//   warps 12..15     epilogue (registers raised with setmaxnreg), one row per thread: tcgen05.ld each finished
 //                    [128 x 64] fp32 chunk accumulator and add it into fp64
 //                    registers; at the end of a tile sum |Delta| (fp64) or store S.
 // The tensor core's fp32 accumulation is not round-to-nearest: accumulating all
 // D/8 * 3 MMA steps of D = 8192 in TMEM biased |Delta| by ~5e-5 (measured on
 // B200).  Restarting the accumulator every 128 columns (48 MMA steps) and
 // carrying the chunk sums in fp64 keeps the error ~1e-6.
-// HBM traffic is the 8 bytes/element of K and K_hat read once (Q stays in L2).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -41,22 +45,47 @@ namespace tc {
 
 constexpr int BM = 128, BN = 64, BK = 32;
 constexpr int KST = 4, QST = 4, AST = 2;
-constexpr int NTHREADS = 320;
-constexpr int CHUNK_KB = 4;  // K-blocks (of 32 columns) per TMEM accumulation chunk
+// warps: 0 producer, 1 MMA (+TMEM alloc), 2-3 idle, 4-11 converters (2 per TMEM lane
+// quarter, 16 columns each), 12-15 epilogue.  Warpgroup 0 gives registers to the
+// epilogue warpgroup (setmaxnreg), which keeps 64 fp64 accumulators per row.
+constexpr int NTHREADS = 512;
+constexpr int NCONV = 256;  // converter threads
+constexpr int CONV_W0 = 4, EPI_W0 = 12;
+constexpr int CHUNK_KB = 4;              // K-blocks (of 32 columns) per TMEM accumulation chunk
+constexpr int CODE_KB = 4;               // K-blocks per code store (128 codes = one 128 B line per row)
 constexpr uint32_t KTILE = BM * BK * 4;  // 16 KB
 constexpr uint32_t QTILE = BN * BK * 4;  // 8 KB (one of hi/lo)
 constexpr uint32_t TMEM_COLS = 256;      // acc 2 x 64 | A ring 2 x (hi 32 + lo 32)
 constexpr uint32_t A_COL0 = 128;
 constexpr uint32_t IDESC = idesc_tf32(BM, BN);
+constexpr int CONV_BAR = 1;  // named barrier id for the NCONV converter threads
+
+// Per K-block quantizer record (fused mode): {s, RN(1/s)} of the 32 columns and a
+// flag set when one of them needs the exact path for every element.
+struct __align__(16) ColRec {
+    float2 c[BK];
+    uint32_t any_exact;
+    uint32_t pad[3];
+};
 
 struct __align__(1024) Smem {
-    uint8_t k[KST][KTILE];
-    uint8_t kh[KST][KTILE];
+    uint8_t k[KST][KTILE];   // K boxes (TMA, 128B swizzle)
+    uint8_t kh[KST][KTILE];  // K_hat boxes (modes 0/1) | fused mode: [0..1] K_hat out staging, [2..3] codes staging
     uint8_t q[QST][2 * QTILE];
+    ColRec cq[KST];          // fused mode: per-column quantizer constants of the K-block
     uint64_t full_k[KST], empty_k[KST], full_q[QST], empty_q[QST];
     uint64_t full_a[AST], empty_a[AST], full_acc[2], empty_acc[2];
     uint32_t tmem_base;
-    double red[3][4];
+    double red[3][8];
+};
+
+struct TcParams {
+    const uint32_t *qsplit;  // pre-split Q tiles (qsplit_kernel)
+    int64_t T, D;
+    int nq, ntiles, nkb, has_khat;
+    Partial *partials;   // MODE 0, 2: one per CTA
+    float *S;            // MODE 1: [nq][T]
+    const ColRec *colq;  // MODE 2: per K-block quantizer records (colq_kernel)
 };
 
 // Q [nq][D] -> per K-block kb: [hi | lo] tiles of BN x BK tf32 in the canonical
@@ -81,26 +110,53 @@ __global__ void qsplit_kernel(const float *__restrict__ Q, int64_t nq, int64_t D
     }
 }
 
-template <int MODE>  // 0: metrics partials (E = K - K_hat), 1: scores S[i][t] (E = K or K - K_hat)
+// Per-K-block quantizer records for the fused kernel: {s, RN(1/s)} per column,
+// with y = 0 for s == 0 (code 0) and for subnormal/huge s, which need the exact
+// path (flagged per block).
+__global__ void colq_kernel(const float *__restrict__ scales, int64_t D, int64_t nkb, ColRec *__restrict__ out) {
+    for (int64_t kb = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; kb < nkb; kb += (int64_t)gridDim.x * blockDim.y) {
+        const int64_t d = kb * BK + threadIdx.x;
+        const float sd = d < D ? scales[d] : 0.0f;
+        const ColQ c = make_colq(sd);
+        out[kb].c[threadIdx.x] = make_float2(sd, c.y);
+        const unsigned any = __ballot_sync(0xffffffffu, c.exact);
+        if (threadIdx.x == 0) {
+            out[kb].any_exact = any ? 1u : 0u;
+            out[kb].pad[0] = out[kb].pad[1] = out[kb].pad[2] = 0u;
+        }
+    }
+}
+
+// byte address of 16-byte chunk c of row r in a [rows][128 B] tile with the TMA 128B swizzle
+__device__ __forceinline__ uint32_t swz(uint32_t base, int r, int c) { return base + r * 128 + ((c ^ (r & 7)) << 4); }
+
+// MODE 0: metrics partials (E = K - K_hat).
+// MODE 1: scores S[i][t] (E = K, or K - K_hat).
+// MODE 2: fused a3+a4+a5+a6: quantize and dequantize the K tile in the
+//         converters (same arithmetic as quant_v4_kernel), write Kq and K_hat,
+//         and contract E = K - K_hat with Q: one HBM pass, 9 bytes/element.
+template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmKh,
-                   const uint32_t *__restrict__ qsplit, int64_t T, int nq, int ntiles, int nkb, int has_khat,
-                   Partial *__restrict__ partials, float *__restrict__ S) {
-    extern __shared__ uint8_t smem_raw[];
-    Smem &s = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+                   const __grid_constant__ CUtensorMap tmKq, const __grid_constant__ TcParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    Smem &s = *reinterpret_cast<Smem *>(smem_raw);
+    const int64_t T = p.T;
+    const int nq = p.nq, ntiles = p.ntiles, nkb = p.nkb, has_khat = p.has_khat;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
     if (threadIdx.x == 0) {
+        if (smem_u32(smem_raw) & 1023u) __trap();  // swizzle atoms need 1024-byte alignment
         for (int i = 0; i < KST; i++) {
             mbar_init(&s.full_k[i], 1);
-            mbar_init(&s.empty_k[i], 128);
+            mbar_init(&s.empty_k[i], NCONV);
         }
         for (int i = 0; i < QST; i++) {
             mbar_init(&s.full_q[i], 1);
             mbar_init(&s.empty_q[i], 1);
         }
         for (int i = 0; i < AST; i++) {
-            mbar_init(&s.full_a[i], 128);
+            mbar_init(&s.full_a[i], NCONV);
             mbar_init(&s.empty_a[i], 1);
         }
         for (int i = 0; i < 2; i++) {
@@ -111,7 +167,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmK);
-        if (has_khat) prefetch_tmap(&tmKh);
+        if (has_khat || MODE == 2) prefetch_tmap(&tmKh);
+        if (MODE == 2) prefetch_tmap(&tmKq);
     }
     if (warp == 1) tmem_alloc<TMEM_COLS>(&s.tmem_base);
     tc_fence_before();
@@ -119,33 +176,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_after();
     const uint32_t tbase = s.tmem_base;
 
-    if (warp == 0) {
-        // ------------------------------------------------------------ producer
-        if (lane == 0) {
+    if (warp < CONV_W0) {
+        setmaxnreg_dec<56>();  // warpgroup 0: producer + MMA issuer need few registers
+        if (warp == 0 && lane == 0) {
+            // ------------------------------------------------------------ producer
             const uint64_t pol_stream = policy_evict_first();
-            const uint64_t pol_q = policy_evict_last();
-            (void)pol_q;
-            const uint32_t kbytes = has_khat ? 2 * KTILE : KTILE;
+            const uint32_t kbytes = (has_khat ? 2 * KTILE : KTILE) + (MODE == 2 ? (uint32_t)sizeof(ColRec) : 0u);
             uint32_t g = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nkb; kb++, g++) {
                     const int sk = g % KST;
-                    const uint32_t pk = (g / KST) & 1;
-                    mbar_wait(&s.empty_k[sk], pk ^ 1);
+                    mbar_wait(&s.empty_k[sk], ((g / KST) & 1) ^ 1);
                     mbar_arrive_tx(&s.full_k[sk], kbytes);
                     tma_load_2d(s.k[sk], &tmK, &s.full_k[sk], kb * BK, tile * BM, pol_stream);
                     if (has_khat) tma_load_2d(s.kh[sk], &tmKh, &s.full_k[sk], kb * BK, tile * BM, pol_stream);
+                    if (MODE == 2) bulk_load(&s.cq[sk], p.colq + kb, sizeof(ColRec), &s.full_k[sk]);
                     const int sq = g % QST;
-                    const uint32_t pq = (g / QST) & 1;
-                    mbar_wait(&s.empty_q[sq], pq ^ 1);
+                    mbar_wait(&s.empty_q[sq], ((g / QST) & 1) ^ 1);
                     mbar_arrive_tx(&s.full_q[sq], 2 * QTILE);
-                    bulk_load(s.q[sq], qsplit + (size_t)kb * (2 * BN * BK), 2 * QTILE, &s.full_q[sq]);
+                    bulk_load(s.q[sq], p.qsplit + (size_t)kb * (2 * BN * BK), 2 * QTILE, &s.full_q[sq]);
                 }
             }
-        }
-    } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        } else if (warp == 1 && lane == 0) {
+            // ------------------------------------------------------------ MMA issuer
             uint32_t g = 0, gc = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nkb; kb++, g++) {
@@ -181,11 +234,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
         }
-    } else if (warp < 6) {
-        // ------------------------------------------------------------ converters (warps 2..5)
+    } else if (warp < EPI_W0) {
+        // ------------------------------------------------------------ converters (warps 4..11)
+        // thread = (row r, half h): columns 16h..16h+15 of every 32-column K-block
         const int quarter = warp & 3;
+        const int h = (warp - CONV_W0) >> 2;
         const int r = quarter * 32 + lane;  // row of the tile == TMEM lane
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+        const bool leader = (warp == CONV_W0 && lane == 0);
         double ss = 0.0;
         float mx = 0.0f;
         uint32_t g = 0;
@@ -193,61 +249,136 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int kb = 0; kb < nkb; kb++, g++) {
                 const int sk = g % KST;
                 mbar_wait(&s.full_k[sk], (g / KST) & 1);
-                const uint8_t *kr = s.k[sk] + r * 128;
-                const uint8_t *hr = s.kh[sk] + r * 128;
-                float e[32];
+                const uint32_t kbase = smem_u32(s.k[sk]);
+                float e[16];
+                if (MODE != 2) {
+                    const uint32_t hbase = smem_u32(s.kh[sk]);
 #pragma unroll
-                for (int c = 0; c < 8; c++) {
-                    const int pos = (c ^ (r & 7)) << 4;  // 128B swizzle: chunk c of row r
-                    const float4 a = *reinterpret_cast<const float4 *>(kr + pos);
-                    float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (has_khat) b = *reinterpret_cast<const float4 *>(hr + pos);
-                    e[4 * c + 0] = __fsub_rn(a.x, b.x);
-                    e[4 * c + 1] = __fsub_rn(a.y, b.y);
-                    e[4 * c + 2] = __fsub_rn(a.z, b.z);
-                    e[4 * c + 3] = __fsub_rn(a.w, b.w);
+                    for (int c = 0; c < 4; c++) {
+                        const float4 a = lds128(swz(kbase, r, 4 * h + c));
+                        float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (has_khat) b = lds128(swz(hbase, r, 4 * h + c));
+                        e[4 * c + 0] = __fsub_rn(a.x, b.x);
+                        e[4 * c + 1] = __fsub_rn(a.y, b.y);
+                        e[4 * c + 2] = __fsub_rn(a.z, b.z);
+                        e[4 * c + 3] = __fsub_rn(a.w, b.w);
+                    }
+                    mbar_arrive(&s.empty_k[sk]);
+                } else {
+                    // ---- a3 + a4 on the resident K row segment (Eq. 7, Eq. 8); same arithmetic and
+                    // exactness argument as quant_v4_kernel (device_common.cuh)
+                    float x[16], v[16], xh[16];
+#pragma unroll
+                    for (int c = 0; c < 4; c++) {
+                        const float4 a = lds128(swz(kbase, r, 4 * h + c));
+                        x[4 * c + 0] = a.x;
+                        x[4 * c + 1] = a.y;
+                        x[4 * c + 2] = a.z;
+                        x[4 * c + 3] = a.w;
+                    }
+                    const uint32_t cqb = smem_u32(&s.cq[sk]) + 16 * h * 8;  // this half's 16 {s, y}
+                    float dmax = 0.0f;
+#pragma unroll
+                    for (int c2 = 0; c2 < 8; c2++) {
+                        const float4 cq = lds128(cqb + 16 * c2);  // {s, y} of 2 columns (broadcast read)
+#pragma unroll
+                        for (int u = 0; u < 2; u++) {
+                            const int i = 2 * c2 + u;
+                            const float sc = u ? cq.z : cq.x, y = u ? cq.w : cq.y;
+                            const float cl = fminf(fmaxf(__fmul_rn(x[i], y), -127.0f), 127.0f);
+                            const float vv = __fadd_rn(cl, kMagic);
+                            const float rr = __fsub_rn(vv, kMagic);
+                            dmax = fmaxf(dmax, fabsf(__fsub_rn(cl, rr)));
+                            v[i] = vv;
+                            xh[i] = __fmul_rn(rr, sc);
+                        }
+                    }
+                    if (dmax > kDangerThr || s.cq[sk].any_exact) {
+                        // rare: a near-tie quotient or an exact-path column -> IEEE division there
+#pragma unroll
+                        for (int i = 0; i < 16; i++) {
+                            const float2 cy = s.cq[sk].c[16 * h + i];
+                            const float cl = fminf(fmaxf(__fmul_rn(x[i], cy.y), -127.0f), 127.0f);
+                            const float rr = __fsub_rn(__fadd_rn(cl, kMagic), kMagic);
+                            if (fabsf(__fsub_rn(cl, rr)) > kDangerThr || (cy.y == 0.0f && cy.x != 0.0f)) {
+                                const int cd = quant_exact(x[i], cy.x);
+                                v[i] = __fadd_rn((float)cd, kMagic);
+                                xh[i] = __fmul_rn((float)cd, cy.x);
+                            }
+                        }
+                    }
+                    mbar_arrive(&s.empty_k[sk]);  // x and the column constants consumed
+                    // Stage K_hat (one [128 x 32] fp32 box per K-block) and the codes (one [128 x 128]
+                    // int8 box per CODE_KB K-blocks) in swizzled smem.  Double-buffered: the leader
+                    // retires the previous block's bulk stores before the barrier below.
+                    const uint32_t khs = smem_u32(s.kh[g & 1]);
+                    const uint32_t cds = smem_u32(s.kh[2 + ((g / CODE_KB) & 1)]);
+#pragma unroll
+                    for (int c = 0; c < 4; c++)
+                        sts128(swz(khs, r, 4 * h + c),
+                               make_float4(xh[4 * c], xh[4 * c + 1], xh[4 * c + 2], xh[4 * c + 3]));
+                    uint4 w;
+                    w.x = pack4(v[0], v[1], v[2], v[3]);
+                    w.y = pack4(v[4], v[5], v[6], v[7]);
+                    w.z = pack4(v[8], v[9], v[10], v[11]);
+                    w.w = pack4(v[12], v[13], v[14], v[15]);
+                    sts128u(swz(cds, r, (kb % CODE_KB) * 2 + h), w);
+                    fence_proxy_async();
+                    if (leader) bulk_wait_read<0>();  // previous block's stores have left smem
+                    named_bar_sync(CONV_BAR, NCONV);
+                    if (leader) {
+                        tma_store_2d(&tmKh, s.kh[g & 1], kb * BK, tile * BM);
+                        if ((kb % CODE_KB) == CODE_KB - 1 || kb == nkb - 1)
+                            tma_store_2d(&tmKq, s.kh[2 + ((g / CODE_KB) & 1)], (kb / CODE_KB) * (BK * CODE_KB),
+                                         tile * BM);
+                        bulk_commit();
+                    }
+#pragma unroll
+                    for (int i = 0; i < 16; i++) e[i] = __fsub_rn(x[i], xh[i]);  // exact (fact 4)
                 }
-                mbar_arrive(&s.empty_k[sk]);
-                if (MODE == 0) {
-                    // each e^2 is exact in fp64; 32 of them summed in fp64 per block
-                    double blk = 0.0;
+                if (MODE != 1) {
+                    // e^2 summed over the 16 columns in fp32, blocks carried in fp64
+                    float blk = 0.0f;
 #pragma unroll
-                    for (int i = 0; i < 32; i++) {
-                        const double ed = (double)e[i];
-                        blk = fma(ed, ed, blk);
+                    for (int i = 0; i < 16; i++) {
+                        blk = fmaf(e[i], e[i], blk);
                         mx = fmaxf(mx, fabsf(e[i]));
                     }
-                    ss += blk;
+                    ss += (double)blk;
                 }
-                uint32_t hi[32], lo[32];
+                // 3xTF32 split: hi = e with the 13 low mantissa bits cleared (a tf32 value),
+                // lo = e - hi exactly (the tensor core reads lo's top 11 bits: error <= 2^-21 |e|)
+                uint32_t hi[16], lo[16];
 #pragma unroll
-                for (int i = 0; i < 32; i++) {
-                    hi[i] = to_tf32(e[i]);
-                    lo[i] = to_tf32(__fsub_rn(e[i], __uint_as_float(hi[i])));
+                for (int i = 0; i < 16; i++) {
+                    hi[i] = __float_as_uint(e[i]) & 0xFFFFE000u;
+                    lo[i] = __float_as_uint(__fsub_rn(e[i], __uint_as_float(hi[i])));
                 }
                 const int sa = g % AST;
                 mbar_wait(&s.empty_a[sa], ((g / AST) & 1) ^ 1);
                 tc_fence_after();
-                tmem_st32(tbase + lane_off + A_COL0 + sa * 64, hi);
-                tmem_st32(tbase + lane_off + A_COL0 + sa * 64 + 32, lo);
+                tmem_st16(tbase + lane_off + A_COL0 + sa * 64 + 16 * h, hi);
+                tmem_st16(tbase + lane_off + A_COL0 + sa * 64 + 32 + 16 * h, lo);
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(&s.full_a[sa]);
             }
         }
-        if (MODE == 0) {
+        if (MODE == 2 && leader) bulk_wait<0>();  // all K_hat / code stores complete
+        if (MODE != 1) {
             double mxd = (double)mx;
             for (int o = 16; o > 0; o >>= 1) {
                 ss += __shfl_xor_sync(0xffffffffu, ss, o);
                 mxd = fmax(mxd, __shfl_xor_sync(0xffffffffu, mxd, o));
             }
             if (lane == 0) {
-                s.red[0][quarter] = ss;
-                s.red[2][quarter] = mxd;
+                s.red[0][warp - CONV_W0] = ss;
+                s.red[2][warp - CONV_W0] = mxd;
             }
         }
     } else {
-        // ------------------------------------------------------------ epilogue (warps 6..9)
+        // ------------------------------------------------------------ epilogue (warps 12..15)
+        setmaxnreg_inc<200>();
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
@@ -264,11 +395,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tc_fence_after();
                 uint32_t v[32];
 #pragma unroll
-                for (int h = 0; h < BN / 32; h++) {
-                    tmem_ld32(tbase + lane_off + ab * BN + 32 * h, v);
+                for (int hh = 0; hh < BN / 32; hh++) {
+                    tmem_ld32(tbase + lane_off + ab * BN + 32 * hh, v);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int j = 0; j < 32; j++) acc[32 * h + j] += (double)__uint_as_float(v[j]);
+                    for (int j = 0; j < 32; j++) acc[32 * hh + j] += (double)__uint_as_float(v[j]);
                 }
                 tc_fence_before();
                 mbar_arrive(&s.empty_acc[ab]);
@@ -278,29 +409,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                 for (int j = 0; j < BN; j++) {
                     if (j < nq) {
-                        if (MODE == 0)
+                        if (MODE != 1)
                             attn += fabs(acc[j]);
                         else
-                            S[(int64_t)j * T + row] = (float)acc[j];
+                            p.S[(int64_t)j * T + row] = (float)acc[j];
                     }
                 }
             }
         }
-        if (MODE == 0) {
+        if (MODE != 1) {
             for (int o = 16; o > 0; o >>= 1) attn += __shfl_xor_sync(0xffffffffu, attn, o);
             if (lane == 0) s.red[1][quarter] = attn;
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (MODE == 0 && threadIdx.x == 0) {
-        Partial p{0.0, 0.0, 0.0, 0.0};
-        for (int i = 0; i < 4; i++) {  // fixed order: deterministic
-            p.sum_sq += s.red[0][i];
-            p.attn_abs += s.red[1][i];
-            p.max_abs = fmax(p.max_abs, s.red[2][i]);
+    if (MODE != 1 && threadIdx.x == 0) {
+        Partial pt{0.0, 0.0, 0.0, 0.0};
+        for (int i = 0; i < 8; i++) {  // fixed order: deterministic
+            pt.sum_sq += s.red[0][i];
+            pt.max_abs = fmax(pt.max_abs, s.red[2][i]);
         }
-        partials[blockIdx.x] = p;
+        for (int i = 0; i < 4; i++) pt.attn_abs += s.red[1][i];
+        p.partials[blockIdx.x] = pt;
     }
     if (warp == 1) {
         tc_fence_after();
@@ -314,26 +445,30 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static std::once_flag once;
     std::call_once(once, [] {
         cudaDriverEntryPointQueryResult q;
-        void *p = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        void *ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
         cudaGetLastError();
     });
     return fn;
 }
 
-static bool make_map(CUtensorMap *m, const float *base, int64_t T, int64_t D) {
+// 2-D row-major [T][D] map, box {box_cols, BM rows}, 128B swizzle (box_cols * elem = 128 B).
+static bool make_map(CUtensorMap *m, const void *base, CUtensorMapDataType ty, int elem, int64_t T, int64_t D,
+                     int box_cols) {
     auto enc = encode_fn();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)T};
-    cuuint64_t strides[1] = {(cuuint64_t)D * 4};
-    cuuint32_t box[2] = {BK, BM};
+    cuuint64_t strides[1] = {(cuuint64_t)D * elem};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, BM};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = enc(m, ty, 2, const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+static bool make_map_f32(CUtensorMap *m, const float *base, int64_t T, int64_t D) {
+    return make_map(m, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, D, BK);
 }
 
 }  // namespace tc
@@ -346,18 +481,41 @@ bool tc_eligible(const float *K, const float *K_hat, int64_t T, int64_t D, int64
 
 size_t tc_qsplit_bytes(int64_t D) { return (size_t)((D + tc::BK - 1) / tc::BK) * 2 * tc::QTILE; }
 
-// Launch: qsplit (into ws_q) + the persistent tensor-core kernel.
+bool tc_roundtrip_eligible(const float *K, const int8_t *Kq, const float *K_hat, int64_t T, int64_t D, int64_t nq) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(K) | reinterpret_cast<uintptr_t>(Kq) |
+                        reinterpret_cast<uintptr_t>(K_hat);
+    return tc_eligible(K, K_hat, T, D, nq) && D % 16 == 0 && (a % 16) == 0;
+}
+
+size_t tc_colq_bytes(int64_t D) { return (size_t)((D + tc::BK - 1) / tc::BK) * sizeof(tc::ColRec); }
+
+template <int MODE>
+static void launch_mode(const CUtensorMap &mK, const CUtensorMap &mKh, const CUtensorMap &mKq, const tc::TcParams &p,
+                        int grid, size_t smem, cudaStream_t s) {
+    static std::once_flag once;
+    std::call_once(once, [&] {
+        cudaFuncSetAttribute(tc::attn_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    tc::attn_tc_kernel<MODE><<<grid, tc::NTHREADS, smem, s>>>(mK, mKh, mKq, p);
+}
+
+// Launch: qsplit (into ws_q) [+ colq] + the persistent tensor-core kernel.
 kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
-                          int64_t nq, void *ws_q, void *partials, int *grid_out, float *S, cudaStream_t s) {
+                          int64_t nq, void *ws_q, void *partials, int *grid_out, float *S, cudaStream_t s,
+                          const float *scales, void *ws_colq, int8_t *Kq_out, float *Kh_out) {
     using namespace tc;
     const int64_t nkb = (D + BK - 1) / BK;
     const int ntiles = (int)((T + BM - 1) / BM);
-    CUtensorMap mK, mKh;
-    if (!make_map(&mK, K, T, D)) return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(K) failed");
-    if (K_hat) {
-        if (!make_map(&mKh, K_hat, T, D)) return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(K_hat) failed");
-    } else {
-        mKh = mK;
+    CUtensorMap mK, mKh, mKq;
+    if (!make_map_f32(&mK, K, T, D)) return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(K) failed");
+    mKh = mK;
+    mKq = mK;
+    if (mode == 2) {
+        if (!make_map_f32(&mKh, Kh_out, T, D)) return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(K_hat) failed");
+        if (!make_map(&mKq, Kq_out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, T, D, BK * CODE_KB))
+            return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(Kq) failed");
+    } else if (K_hat) {
+        if (!make_map_f32(&mKh, K_hat, T, D)) return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(K_hat) failed");
     }
     uint32_t *qs = reinterpret_cast<uint32_t *>(ws_q);
     {
@@ -366,25 +524,32 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
         qsplit_kernel<<<blocks, 256, 0, s>>>(Q, nq, D, nkb, qs);
         if (kvq_status st = check_launch("qsplit"); st != KVQ_OK) return st;
     }
-    const int grid = std::min(ntiles, device_info().num_sms);
-    const size_t smem = sizeof(Smem) + 1024;
-    if (grid_out) *grid_out = grid;
-    if (mode == 0) {
-        static std::once_flag once;
-        std::call_once(once, [&] {
-            cudaFuncSetAttribute(attn_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        });
-        attn_tc_kernel<0><<<grid, NTHREADS, smem, s>>>(mK, mKh, qs, T, (int)nq, ntiles, (int)nkb, K_hat != nullptr,
-                                                        reinterpret_cast<Partial *>(partials), nullptr);
-    } else {
-        static std::once_flag once;
-        std::call_once(once, [&] {
-            cudaFuncSetAttribute(attn_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        });
-        attn_tc_kernel<1><<<grid, NTHREADS, smem, s>>>(mK, mKh, qs, T, (int)nq, ntiles, (int)nkb, K_hat != nullptr,
-                                                        nullptr, S);
+    TcParams p{};
+    p.qsplit = qs;
+    p.T = T;
+    p.D = D;
+    p.nq = (int)nq;
+    p.ntiles = ntiles;
+    p.nkb = (int)nkb;
+    p.has_khat = (K_hat != nullptr && mode != 2);
+    p.partials = reinterpret_cast<Partial *>(partials);
+    p.S = S;
+    if (mode == 2) {
+        ColRec *cq = reinterpret_cast<ColRec *>(ws_colq);
+        colq_kernel<<<(unsigned)std::min<int64_t>((nkb + 7) / 8, 1024), dim3(32, 8), 0, s>>>(scales, D, nkb, cq);
+        if (kvq_status st = check_launch("colq"); st != KVQ_OK) return st;
+        p.colq = cq;
     }
-    return check_launch(mode == 0 ? "attn_tc(metrics)" : "attn_tc(scores)");
+    const int grid = std::min(ntiles, device_info().num_sms);
+    const size_t smem = sizeof(Smem);
+    if (grid_out) *grid_out = grid;
+    if (mode == 0)
+        launch_mode<0>(mK, mKh, mKq, p, grid, smem, s);
+    else if (mode == 1)
+        launch_mode<1>(mK, mKh, mKq, p, grid, smem, s);
+    else
+        launch_mode<2>(mK, mKh, mKq, p, grid, smem, s);
+    return check_launch(mode == 0 ? "attn_tc(metrics)" : mode == 1 ? "attn_tc(scores)" : "attn_tc(roundtrip)");
 }
 
 }  // namespace kvq

@@ -44,16 +44,6 @@ kvq_status launch_dequantize(const int8_t *Kq, const float *scales, int64_t T, i
                              cudaStream_t s);
 
 // ---- metrics kernels (metrics_kernels.cu, attn_tc.cu)
-struct Partial {  // per-CTA partial sums of a5/a6
-    double sum_sq, attn_abs, max_abs, pad;
-};
-bool tc_eligible(const float *K, const float *K_hat, int64_t T, int64_t D, int64_t nq);
-size_t tc_qsplit_bytes(int64_t D);
-// mode 0: write per-CTA Partials (grid returned in *grid_out); mode 1: write S [nq][T].
-kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
-                          int64_t nq, void *ws_q, void *partials, int *grid_out, float *S, cudaStream_t s);
-bool force_simt();  // KVQ_FORCE_SIMT=1: use the CUDA-core attention kernel (tests compare the two)
-size_t metrics_workspace_size(int64_t T, int64_t D, int64_t nq);
 // Writes per-rank totals {sum_sq, attn_abs_sum, n_elems, n_scores} (double[4]) and
 // {max_abs_bits, theo_max_bits} (uint64[2]) into the workspace tail; returns
 // pointers to them so the comm layer can all-reduce in place.
@@ -61,6 +51,25 @@ struct MetricTotals {
     double *sums;      // [4] device
     uint64_t *maxes;   // [2] device
 };
+struct Partial {  // per-CTA partial sums of a5/a6
+    double sum_sq, attn_abs, max_abs, pad;
+};
+bool tc_eligible(const float *K, const float *K_hat, int64_t T, int64_t D, int64_t nq);
+size_t tc_qsplit_bytes(int64_t D);
+// mode 0: write per-CTA Partials (grid returned in *grid_out); mode 1: write S [nq][T].
+bool tc_roundtrip_eligible(const float *K, const int8_t *Kq, const float *K_hat, int64_t T, int64_t D, int64_t nq);
+size_t tc_colq_bytes(int64_t D);
+// mode 2: fused a3+a4+a5+a6 (needs scales, colq workspace, Kq/Kh outputs).
+kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
+                          int64_t nq, void *ws_q, void *partials, int *grid_out, float *S, cudaStream_t s,
+                          const float *scales = nullptr, void *ws_colq = nullptr, int8_t *Kq_out = nullptr,
+                          float *Kh_out = nullptr);
+// a3+a4+a5+a6 in one pass when eligible, else quantize_dequantize + metrics kernels.
+kvq_status launch_roundtrip_partials(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
+                                     float *K_hat, const float *Q, int64_t nq, void *ws, size_t ws_bytes,
+                                     MetricTotals *totals, cudaStream_t s);
+bool force_simt();  // KVQ_FORCE_SIMT=1: use the CUDA-core attention kernel (tests compare the two)
+size_t metrics_workspace_size(int64_t T, int64_t D, int64_t nq);
 kvq_status launch_metrics_partials(const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
                                    int64_t nq, const float *scales, void *ws, size_t ws_bytes,
                                    MetricTotals *totals, cudaStream_t s);

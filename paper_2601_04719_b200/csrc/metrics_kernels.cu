@@ -232,11 +232,45 @@ bool force_simt() {
 
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// workspace: [partials (max(simt tiles, 1024 CTAs)) | Q split tiles | totals]
+// workspace: [partials (max(simt tiles, 1024 CTAs)) | Q split tiles | column constants | totals]
+struct WsLayout {
+    Partial *partials;
+    void *qsplit;
+    void *colq;
+    double *sums;
+    uint64_t *maxes;
+};
+
+static WsLayout ws_layout(void *ws, int64_t T, int64_t D) {
+    const uintptr_t base = (reinterpret_cast<uintptr_t>(ws) + 255) & ~(uintptr_t)255;
+    const size_t np = (size_t)std::max<int64_t>(num_tiles(T), 1024);
+    WsLayout L;
+    uintptr_t off = base;
+    L.partials = reinterpret_cast<Partial *>(off);
+    off += al256(np * sizeof(Partial));
+    L.qsplit = reinterpret_cast<void *>(off);
+    off += al256(tc_qsplit_bytes(D));
+    L.colq = reinterpret_cast<void *>(off);
+    off += al256(tc_colq_bytes(D));
+    L.sums = reinterpret_cast<double *>(off);
+    L.maxes = reinterpret_cast<uint64_t *>(L.sums + 4);
+    return L;
+}
+
 size_t metrics_workspace_size(int64_t T, int64_t D, int64_t nq) {
     (void)nq;
     const size_t np = (size_t)std::max<int64_t>(num_tiles(T), 1024);
-    return 256 + al256(np * sizeof(Partial)) + al256(tc_qsplit_bytes(D)) + 4 * sizeof(double) + 2 * sizeof(uint64_t);
+    return 256 + al256(np * sizeof(Partial)) + al256(tc_qsplit_bytes(D)) + al256(tc_colq_bytes(D)) +
+           4 * sizeof(double) + 2 * sizeof(uint64_t);
+}
+
+static kvq_status reduce_partials(const WsLayout &L, int64_t nparts, const float *scales, int64_t T, int64_t D,
+                                  int64_t nq, MetricTotals *totals, cudaStream_t s) {
+    totals->sums = L.sums;
+    totals->maxes = L.maxes;
+    reduce_partials_kernel<<<1, 1024, 0, s>>>(L.partials, nparts, scales, D, (double)T * (double)D,
+                                              (double)nq * (double)T, L.sums, L.maxes);
+    return check_launch("metrics_reduce");
 }
 
 kvq_status launch_metrics_partials(const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
@@ -244,27 +278,39 @@ kvq_status launch_metrics_partials(const float *K, const float *K_hat, int64_t T
                                    MetricTotals *totals, cudaStream_t s) {
     if (ws_bytes < metrics_workspace_size(T, D, nq))
         return fail(KVQ_ERR_INVALID_VALUE, "error_metrics: workspace too small");
-    uintptr_t base = (reinterpret_cast<uintptr_t>(ws) + 255) & ~(uintptr_t)255;
-    Partial *partials = reinterpret_cast<Partial *>(base);
-    const size_t np = (size_t)std::max<int64_t>(num_tiles(T), 1024);
-    void *qsplit = reinterpret_cast<void *>(base + al256(np * sizeof(Partial)));
-    totals->sums = reinterpret_cast<double *>(base + al256(np * sizeof(Partial)) + al256(tc_qsplit_bytes(D)));
-    totals->maxes = reinterpret_cast<uint64_t *>(totals->sums + 4);
+    const WsLayout L = ws_layout(ws, T, D);
     int64_t nparts;
     if (!force_simt() && tc_eligible(K, K_hat, T, D, nq)) {
         int grid = 0;
-        if (kvq_status st = launch_attn_tc(0, K, K_hat, T, D, Q, nq, qsplit, partials, &grid, nullptr, s);
+        if (kvq_status st = launch_attn_tc(0, K, K_hat, T, D, Q, nq, L.qsplit, L.partials, &grid, nullptr, s);
             st != KVQ_OK)
             return st;
         nparts = grid;
     } else {
         nparts = num_tiles(T);
-        attn_tile_kernel<0><<<(unsigned)nparts, 256, 0, s>>>(K, K_hat, Q, T, D, nq, partials, nullptr);
+        attn_tile_kernel<0><<<(unsigned)nparts, 256, 0, s>>>(K, K_hat, Q, T, D, nq, L.partials, nullptr);
         if (kvq_status st = check_launch("metrics_tiles"); st != KVQ_OK) return st;
     }
-    reduce_partials_kernel<<<1, 1024, 0, s>>>(partials, nparts, scales, D, (double)T * (double)D,
-                                              (double)nq * (double)T, totals->sums, totals->maxes);
-    return check_launch("metrics_reduce");
+    return reduce_partials(L, nparts, scales, T, D, nq, totals, s);
+}
+
+kvq_status launch_roundtrip_partials(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
+                                     float *K_hat, const float *Q, int64_t nq, void *ws, size_t ws_bytes,
+                                     MetricTotals *totals, cudaStream_t s) {
+    if (ws_bytes < metrics_workspace_size(T, D, nq))
+        return fail(KVQ_ERR_INVALID_VALUE, "roundtrip: workspace too small");
+    if (!force_simt() && tc_roundtrip_eligible(K, Kq, K_hat, T, D, nq)) {
+        const WsLayout L = ws_layout(ws, T, D);
+        int grid = 0;
+        if (kvq_status st = launch_attn_tc(2, K, nullptr, T, D, Q, nq, L.qsplit, L.partials, &grid, nullptr, s,
+                                           scales, L.colq, Kq, K_hat);
+            st != KVQ_OK)
+            return st;
+        return reduce_partials(L, grid, scales, T, D, nq, totals, s);
+    }
+    // not eligible for the single pass: fused quantize+dequantize, then the metrics pass
+    if (kvq_status st = launch_quantize(K, scales, T, D, Kq, K_hat, s); st != KVQ_OK) return st;
+    return launch_metrics_partials(K, K_hat, T, D, Q, nq, scales, ws, ws_bytes, totals, s);
 }
 
 kvq_status launch_metrics_finalize(const MetricTotals &t, kvq_metrics *out_dev, cudaStream_t s) {

@@ -17,7 +17,7 @@ __all__ = [
     "KvqError", "Comm", "kvq_compute_scales", "kvq_quantize", "kvq_dequantize", "kvq_quantize_dequantize",
     "kvq_error_metrics", "kvq_error_metrics_async", "kvq_error_metrics_workspace_size", "kvq_attention_scores",
     "kvq_roundtrip_host", "kvq_roundtrip_host_workspace_size", "kvq_synth_fill", "kvq_device_check",
-    "kvq_comm_unique_id", "METRICS_BYTES", "metrics_from_device",
+    "kvq_comm_unique_id", "METRICS_BYTES", "metrics_from_device", "kvq_roundtrip", "kvq_roundtrip_workspace_size",
 ]
 
 load()  # fail loudly at import if libkvq.so cannot be loaded or built
@@ -183,6 +183,40 @@ def kvq_error_metrics(K, K_hat, Q=None, scales=None, workspace=None, comm: Optio
                                    workspace.numel(), _comm_handle(comm), ctypes.byref(out), _stream(stream)),
           "kvq_error_metrics")
     return out.to_dict()
+
+
+def kvq_roundtrip_workspace_size(T: int, D: int, nq: int) -> int:
+    return int(load().kvq_roundtrip_workspace_size(T, D, nq))
+
+
+def kvq_roundtrip(K: torch.Tensor, scales: torch.Tensor, Q: Optional[torch.Tensor] = None,
+                  Kq: Optional[torch.Tensor] = None, K_hat: Optional[torch.Tensor] = None,
+                  out_dev: Optional[torch.Tensor] = None, workspace=None, comm: Optional[Comm] = None,
+                  stream=None):
+    """a3+a4+a5+a6 in one HBM pass.  Returns (Kq, K_hat, out_dev) with out_dev a
+    device kvq_metrics (read it with metrics_from_device)."""
+    T, D = _mat(K, torch.float32, "K")
+    _vec(scales, D, "scales")
+    nq = 0
+    if Q is not None:
+        nq, Dq = _mat(Q, torch.float32, "Q")
+        assert Dq == D
+    if Kq is None:
+        Kq = torch.empty((T, D), dtype=torch.int8, device=K.device)
+    if K_hat is None:
+        K_hat = torch.empty((T, D), dtype=torch.float32, device=K.device)
+    _mat(Kq, torch.int8, "Kq")
+    _mat(K_hat, torch.float32, "K_hat")
+    need = kvq_roundtrip_workspace_size(T, D, nq)
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=K.device)
+    assert workspace.numel() >= need, "workspace too small"
+    if out_dev is None:
+        out_dev = torch.empty(METRICS_BYTES, dtype=torch.uint8, device=K.device)
+    check(load().kvq_roundtrip(_ptr(K), _ptr(scales), T, D, _ptr(Kq), _ptr(K_hat), _ptr(Q), nq, _ptr(workspace),
+                               workspace.numel(), _comm_handle(comm), _ptr(out_dev), _stream(stream)),
+          "kvq_roundtrip")
+    return Kq, K_hat, out_dev
 
 
 def kvq_attention_scores(Q: torch.Tensor, K: torch.Tensor, K_hat: Optional[torch.Tensor] = None,

@@ -1,5 +1,4 @@
 set -x
-nvidia-smi -L
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -3 gpurun_out/smoke.log
-timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "tc or scores" > gpurun_out/pytest_tc.log 2>&1; tail -30 gpurun_out/pytest_tc.log
-timeout 400 python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench2.log 2>&1; tail -5 gpurun_out/bench2.log
+python scripts/diag_rt.py 1024 2>&1 | tail -12
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_all.log 2>&1; tail -8 gpurun_out/pytest_all.log
+timeout 400 python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_fused.log 2>&1; tail -1 gpurun_out/bench_fused.log | grep -o '"ms_per_step.*"roofline"'
