@@ -34,6 +34,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "device_common.cuh"
@@ -44,8 +45,16 @@ namespace kvq {
 namespace tc {
 
 constexpr int BM = 128, BN = 64, BK = 32;
-constexpr int KST = 4, QST = 4, AST = 2;
-// warps: 0 producer, 1 MMA (+TMEM alloc), 2-3 idle, 4-11 converters (2 per TMEM lane
+constexpr int QST = 4, AST = 4;
+// Input ring: modes 0/1 stage K and K_hat (32 KB) x 4; the fused mode stages K only
+// (16 KB) x 8, i.e. 128 KB in flight per SM either way (Little's law at ~44 GB/s/SM).
+constexpr int KST_MAX = 8;
+template <int MODE>
+struct Ring {
+    static constexpr int kst = MODE == 2 ? 8 : 4;
+    static constexpr uint32_t stage = MODE == 2 ? 16384u : 32768u;
+};
+// warps: 0 K producer, 1 MMA (+TMEM alloc), 2 output stores (fused mode), 3 Q producer, 4-11 converters (2 per TMEM lane
 // quarter, 16 columns each), 12-15 epilogue.  Warpgroup 0 gives registers to the
 // epilogue warpgroup (setmaxnreg), which keeps 64 fp64 accumulators per row.
 constexpr int NTHREADS = 512;
@@ -55,10 +64,9 @@ constexpr int CHUNK_KB = 4;              // K-blocks (of 32 columns) per TMEM ac
 constexpr int CODE_KB = 4;               // K-blocks per code store (128 codes = one 128 B line per row)
 constexpr uint32_t KTILE = BM * BK * 4;  // 16 KB
 constexpr uint32_t QTILE = BN * BK * 4;  // 8 KB (one of hi/lo)
-constexpr uint32_t TMEM_COLS = 256;      // acc 2 x 64 | A ring 2 x (hi 32 + lo 32)
+constexpr uint32_t TMEM_COLS = 512;      // acc 2 x 64 | A ring AST x (hi 32 + lo 32) (| 128 spare)
 constexpr uint32_t A_COL0 = 128;
 constexpr uint32_t IDESC = idesc_tf32(BM, BN);
-constexpr int CONV_BAR = 1;  // named barrier id for the NCONV converter threads
 
 // Per K-block quantizer record (fused mode): {s, RN(1/s)} of the 32 columns and a
 // flag set when one of them needs the exact path for every element.
@@ -69,15 +77,21 @@ struct __align__(16) ColRec {
 };
 
 struct __align__(1024) Smem {
-    uint8_t k[KST][KTILE];   // K boxes (TMA, 128B swizzle)
-    uint8_t kh[KST][KTILE];  // K_hat boxes (modes 0/1) | fused mode: [0..1] K_hat out staging, [2..3] codes staging
+    // modes 0/1: stage i = [K box | K_hat box] at 32 KB * i (4 stages)
+    // fused:     stage i = K box at 16 KB * i (8 stages; the converters overwrite it in place with
+    //            the K_hat box, which the store warp writes out before the stage is refilled),
+    //            codes staging at 128 KB + 16 KB * b (b = 0, 1)
+    uint8_t buf[160 * 1024];
     uint8_t q[QST][2 * QTILE];
-    ColRec cq[KST];          // fused mode: per-column quantizer constants of the K-block
-    uint64_t full_k[KST], empty_k[KST], full_q[QST], empty_q[QST];
+    ColRec cq[KST_MAX];      // fused mode: per-column quantizer constants of the K-block
+    uint64_t full_k[KST_MAX], empty_k[KST_MAX], full_q[QST], empty_q[QST];
     uint64_t full_a[AST], empty_a[AST], full_acc[2], empty_acc[2];
+    uint64_t staged[KST_MAX], cstored[2];  // fused mode: handoff converters -> store warp -> converters
     uint32_t tmem_base;
     double red[3][8];
 };
+
+static_assert(sizeof(Smem) <= 227 * 1024, "shared memory budget (227 KB per CTA on sm_100)");
 
 struct TcParams {
     const uint32_t *qsplit;  // pre-split Q tiles (qsplit_kernel)
@@ -86,6 +100,8 @@ struct TcParams {
     Partial *partials;   // MODE 0, 2: one per CTA
     float *S;            // MODE 1: [nq][T]
     const ColRec *colq;  // MODE 2: per K-block quantizer records (colq_kernel)
+    int store_hint;      // unused (kept for experiments)
+    float *Kh;           // MODE 2: K_hat output [T][D]
 };
 
 // Q [nq][D] -> per K-block kb: [hi | lo] tiles of BN x BK tf32 in the canonical
@@ -144,12 +160,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int64_t T = p.T;
     const int nq = p.nq, ntiles = p.ntiles, nkb = p.nkb, has_khat = p.has_khat;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    constexpr int KST = Ring<MODE>::kst;
 
     if (threadIdx.x == 0) {
         if (smem_u32(smem_raw) & 1023u) __trap();  // swizzle atoms need 1024-byte alignment
-        for (int i = 0; i < KST; i++) {
+        for (int i = 0; i < Ring<MODE>::kst; i++) {
             mbar_init(&s.full_k[i], 1);
-            mbar_init(&s.empty_k[i], NCONV);
+            mbar_init(&s.empty_k[i], MODE == 2 ? 1 : NCONV);  // fused: the store warp frees the stage
+            mbar_init(&s.staged[i], NCONV);
         }
         for (int i = 0; i < QST; i++) {
             mbar_init(&s.full_q[i], 1);
@@ -163,6 +181,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(&s.full_acc[i], 1);
             mbar_init(&s.empty_acc[i], 128);
         }
+        for (int i = 0; i < 2; i++) mbar_init(&s.cstored[i], 1);
         mbar_fence_init();
     }
     if (warp == 0 && lane == 0) {
@@ -181,6 +200,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (warp == 0 && lane == 0) {
             // ------------------------------------------------------------ producer
             const uint64_t pol_stream = policy_evict_first();
+            const uint64_t pol_keep = policy_evict_last();  // Q tiles / column records: re-read by every tile
             const uint32_t kbytes = (has_khat ? 2 * KTILE : KTILE) + (MODE == 2 ? (uint32_t)sizeof(ColRec) : 0u);
             uint32_t g = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -188,15 +208,54 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const int sk = g % KST;
                     mbar_wait(&s.empty_k[sk], ((g / KST) & 1) ^ 1);
                     mbar_arrive_tx(&s.full_k[sk], kbytes);
-                    tma_load_2d(s.k[sk], &tmK, &s.full_k[sk], kb * BK, tile * BM, pol_stream);
-                    if (has_khat) tma_load_2d(s.kh[sk], &tmKh, &s.full_k[sk], kb * BK, tile * BM, pol_stream);
-                    if (MODE == 2) bulk_load(&s.cq[sk], p.colq + kb, sizeof(ColRec), &s.full_k[sk]);
+                    uint8_t *stg = s.buf + sk * Ring<MODE>::stage;
+                    tma_load_2d(stg, &tmK, &s.full_k[sk], kb * BK, tile * BM, pol_stream);
+                    if (has_khat) tma_load_2d(stg + KTILE, &tmKh, &s.full_k[sk], kb * BK, tile * BM, pol_stream);
+                    if (MODE == 2) bulk_load(&s.cq[sk], p.colq + kb, sizeof(ColRec), &s.full_k[sk], pol_keep);
+                }
+            }
+        } else if (warp == 3 && lane == 0) {
+            // ------------------------------------------------------------ Q producer (L2-resident tiles)
+            // Separate from the K producer so a late MMA never holds back the HBM stream.
+            const uint64_t pol_keep = policy_evict_last();
+            uint32_t g = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int kb = 0; kb < nkb; kb++, g++) {
                     const int sq = g % QST;
                     mbar_wait(&s.empty_q[sq], ((g / QST) & 1) ^ 1);
                     mbar_arrive_tx(&s.full_q[sq], 2 * QTILE);
-                    bulk_load(s.q[sq], p.qsplit + (size_t)kb * (2 * BN * BK), 2 * QTILE, &s.full_q[sq]);
+                    bulk_load(s.q[sq], p.qsplit + (size_t)kb * (2 * BN * BK), 2 * QTILE, &s.full_q[sq], pol_keep);
                 }
             }
+        } else if (MODE == 2 && warp == 2 && lane == 0) {
+            // ------------------------------------------------------------ output store warp (fused mode)
+            // K-block g's K_hat box has been written by the converters into its own input stage
+            // (g % KST); every CODE_KB blocks the group's codes ([128 rows x 128 B], full lines: no
+            // DRAM read-modify-write) sit in code buffer grp & 1.  Store them with TMA; one block
+            // later, when the bulk engine has read them out of smem, free the input stage for the
+            // producer and (at group ends) the code buffer for the converters.
+            uint32_t g = 0, grp = 0;
+            bool prev_group_end = false;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int kb = 0; kb < nkb; kb++, g++) {
+                    const int sk = g % KST;
+                    mbar_wait(&s.staged[sk], (g / KST) & 1);
+                    tma_store_2d(&tmKh, s.buf + sk * Ring<MODE>::stage, kb * BK, tile * BM, policy_evict_normal());
+                    const bool group_end = (kb % CODE_KB) == CODE_KB - 1 || kb == nkb - 1;
+                    if (group_end)
+                        tma_store_2d(&tmKq, s.buf + 128 * 1024 + (grp & 1) * KTILE, (kb / CODE_KB) * (BK * CODE_KB),
+                                     tile * BM, policy_evict_normal());
+                    bulk_commit();
+                    if (g > 0) {
+                        bulk_wait_read<1>();  // block g-1's boxes have left smem
+                        mbar_arrive(&s.empty_k[(g - 1) % KST]);
+                        if (prev_group_end) mbar_arrive(&s.cstored[(grp - 1) & 1]);
+                    }
+                    prev_group_end = group_end;
+                    if (group_end) grp++;
+                }
+            }
+            bulk_wait<0>();  // all K_hat / code writes complete before the CTA retires
         } else if (warp == 1 && lane == 0) {
             // ------------------------------------------------------------ MMA issuer
             uint32_t g = 0, gc = 0;
@@ -241,18 +300,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int h = (warp - CONV_W0) >> 2;
         const int r = quarter * 32 + lane;  // row of the tile == TMEM lane
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-        const bool leader = (warp == CONV_W0 && lane == 0);
         double ss = 0.0;
         float mx = 0.0f;
-        uint32_t g = 0;
+        uint32_t g = 0, cgrp = 0;  // K-block and code-group counters (same order as the store warp)
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             for (int kb = 0; kb < nkb; kb++, g++) {
                 const int sk = g % KST;
                 mbar_wait(&s.full_k[sk], (g / KST) & 1);
-                const uint32_t kbase = smem_u32(s.k[sk]);
+                const uint32_t kbase = smem_u32(s.buf + sk * Ring<MODE>::stage);
                 float e[16];
                 if (MODE != 2) {
-                    const uint32_t hbase = smem_u32(s.kh[sk]);
+                    const uint32_t hbase = kbase + KTILE;
 #pragma unroll
                     for (int c = 0; c < 4; c++) {
                         const float4 a = lds128(swz(kbase, r, 4 * h + c));
@@ -307,15 +365,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             }
                         }
                     }
-                    mbar_arrive(&s.empty_k[sk]);  // x and the column constants consumed
-                    // Stage K_hat (one [128 x 32] fp32 box per K-block) and the codes (one [128 x 128]
-                    // int8 box per CODE_KB K-blocks) in swizzled smem.  Double-buffered: the leader
-                    // retires the previous block's bulk stores before the barrier below.
-                    const uint32_t khs = smem_u32(s.kh[g & 1]);
-                    const uint32_t cds = smem_u32(s.kh[2 + ((g / CODE_KB) & 1)]);
+                    // K_hat overwrites x in the input stage (same swizzled positions, read by this
+                    // thread only); the codes go to the group's code buffer.  The store warp writes
+                    // both out with TMA and then frees the stage (and the code buffer).
+                    if ((kb % CODE_KB) == 0) mbar_wait(&s.cstored[cgrp & 1], ((cgrp >> 1) & 1) ^ 1);
+                    const uint32_t cds = smem_u32(s.buf + 128 * 1024 + (cgrp & 1) * KTILE);
 #pragma unroll
                     for (int c = 0; c < 4; c++)
-                        sts128(swz(khs, r, 4 * h + c),
+                        sts128(swz(kbase, r, 4 * h + c),
                                make_float4(xh[4 * c], xh[4 * c + 1], xh[4 * c + 2], xh[4 * c + 3]));
                     uint4 w;
                     w.x = pack4(v[0], v[1], v[2], v[3]);
@@ -323,16 +380,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     w.z = pack4(v[8], v[9], v[10], v[11]);
                     w.w = pack4(v[12], v[13], v[14], v[15]);
                     sts128u(swz(cds, r, (kb % CODE_KB) * 2 + h), w);
-                    fence_proxy_async();
-                    if (leader) bulk_wait_read<0>();  // previous block's stores have left smem
-                    named_bar_sync(CONV_BAR, NCONV);
-                    if (leader) {
-                        tma_store_2d(&tmKh, s.kh[g & 1], kb * BK, tile * BM);
-                        if ((kb % CODE_KB) == CODE_KB - 1 || kb == nkb - 1)
-                            tma_store_2d(&tmKq, s.kh[2 + ((g / CODE_KB) & 1)], (kb / CODE_KB) * (BK * CODE_KB),
-                                         tile * BM);
-                        bulk_commit();
-                    }
+                    fence_proxy_async();  // generic smem writes -> visible to the TMA (async proxy)
+                    mbar_arrive(&s.staged[sk]);
+                    if ((kb % CODE_KB) == CODE_KB - 1 || kb == nkb - 1) cgrp++;
 #pragma unroll
                     for (int i = 0; i < 16; i++) e[i] = __fsub_rn(x[i], xh[i]);  // exact (fact 4)
                 }
@@ -364,7 +414,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 mbar_arrive(&s.full_a[sa]);
             }
         }
-        if (MODE == 2 && leader) bulk_wait<0>();  // all K_hat / code stores complete
         if (MODE != 1) {
             double mxd = (double)mx;
             for (int o = 16; o > 0; o >>= 1) {
@@ -534,11 +583,16 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
     p.has_khat = (K_hat != nullptr && mode != 2);
     p.partials = reinterpret_cast<Partial *>(partials);
     p.S = S;
+    {
+        const char *e = std::getenv("KVQ_TC_STORE_HINT");
+        p.store_hint = e ? std::atoi(e) : 0;
+    }
     if (mode == 2) {
         ColRec *cq = reinterpret_cast<ColRec *>(ws_colq);
         colq_kernel<<<(unsigned)std::min<int64_t>((nkb + 7) / 8, 1024), dim3(32, 8), 0, s>>>(scales, D, nkb, cq);
         if (kvq_status st = check_launch("colq"); st != KVQ_OK) return st;
         p.colq = cq;
+        p.Kh = Kh_out;
     }
     const int grid = std::min(ntiles, device_info().num_sms);
     const size_t smem = sizeof(Smem);
