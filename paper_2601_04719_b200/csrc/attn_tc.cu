@@ -100,7 +100,8 @@ struct TcParams {
     Partial *partials;   // MODE 0, 2: one per CTA
     float *S;            // MODE 1: [nq][T]
     const ColRec *colq;  // MODE 2: per K-block quantizer records (colq_kernel)
-    int store_hint;      // unused (kept for experiments)
+    int hints;           // L2 policies: bit0 K loads evict-first, bit1 output stores evict-first (default both;
+                         // evict-first loads with normal stores cost ~0.6 GB of extra DRAM reads at C4)
     float *Kh;           // MODE 2: K_hat output [T][D]
 };
 
@@ -199,8 +200,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         setmaxnreg_dec<56>();  // warpgroup 0: producer + MMA issuer need few registers
         if (warp == 0 && lane == 0) {
             // ------------------------------------------------------------ producer
-            const uint64_t pol_stream = policy_evict_first();
-            const uint64_t pol_keep = policy_evict_last();  // Q tiles / column records: re-read by every tile
+            const uint64_t pol_stream = (p.hints & 1) ? policy_evict_first() : policy_evict_normal();
+            const uint64_t pol_keep = policy_evict_last();  // column records: re-read by every tile
             const uint32_t kbytes = (has_khat ? 2 * KTILE : KTILE) + (MODE == 2 ? (uint32_t)sizeof(ColRec) : 0u);
             uint32_t g = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -234,17 +235,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // DRAM read-modify-write) sit in code buffer grp & 1.  Store them with TMA; one block
             // later, when the bulk engine has read them out of smem, free the input stage for the
             // producer and (at group ends) the code buffer for the converters.
+            const uint64_t pol_out = (p.hints & 2) ? policy_evict_first() : policy_evict_normal();
             uint32_t g = 0, grp = 0;
             bool prev_group_end = false;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nkb; kb++, g++) {
                     const int sk = g % KST;
                     mbar_wait(&s.staged[sk], (g / KST) & 1);
-                    tma_store_2d(&tmKh, s.buf + sk * Ring<MODE>::stage, kb * BK, tile * BM, policy_evict_normal());
+                    tma_store_2d(&tmKh, s.buf + sk * Ring<MODE>::stage, kb * BK, tile * BM, pol_out);
                     const bool group_end = (kb % CODE_KB) == CODE_KB - 1 || kb == nkb - 1;
                     if (group_end)
                         tma_store_2d(&tmKq, s.buf + 128 * 1024 + (grp & 1) * KTILE, (kb / CODE_KB) * (BK * CODE_KB),
-                                     tile * BM, policy_evict_normal());
+                                     tile * BM, pol_out);
                     bulk_commit();
                     if (g > 0) {
                         bulk_wait_read<1>();  // block g-1's boxes have left smem
@@ -584,8 +586,8 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
     p.partials = reinterpret_cast<Partial *>(partials);
     p.S = S;
     {
-        const char *e = std::getenv("KVQ_TC_STORE_HINT");
-        p.store_hint = e ? std::atoi(e) : 0;
+        const char *e = std::getenv("KVQ_TC_HINTS");  // experiments only
+        p.hints = e ? std::atoi(e) : 3;
     }
     if (mode == 2) {
         ColRec *cq = reinterpret_cast<ColRec *>(ws_colq);
