@@ -38,6 +38,18 @@ METRIC = "quantize+dequantize elements/s and achieved HBM GB/s vs B200 peak at 1
 BYTES = {"scales": 4, "quantize": 5, "dequantize": 5, "metrics": 8, "roundtrip": 9}
 
 
+def measured_traffic(kernel: str):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of `kernel`
+    from the committed `ncu --set full` capture summary (profiles/traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        j = json.load(f)
+    v = j.get("kernels", {}).get(kernel)
+    return None if v is None else {"bytes_per_launch": v["bytes"], "source": j.get("source"), "config": v.get("config")}
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -148,7 +160,7 @@ def run_reference(args, cfg, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (splitmix64 lattice uniform [-1,1), SURVEY §8(d))",
-            "config": {"workload": cfg["desc"], "T": cfg["T"], "D": cfg["D"], "nq": cfg["nq"]},
+            "config": {"workload": f"{cfg['name']}: {cfg['desc']}", "T": cfg["T"], "D": cfg["D"], "nq": cfg["nq"]},
             "cpu_baseline": {"value": value, "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -287,9 +299,12 @@ def run_kvq(args, cfg, rank, world, local_rank):
     if dom:
         t = passes[dom]
         ach = BYTES[dom] * n_local / (t * 1e-3) / 1e9
+        tr = measured_traffic(dom) if args.config == "C4" and world == 1 else None
         roofline = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": ach / pk["hbm_gbs"], "traffic": None, "peak_source": pk["source"],
-                    "algo_bytes_per_elem": BYTES[dom], "ms_per_launch": t}
+                    "frac": ach / pk["hbm_gbs"], "traffic": None if tr is None else tr["bytes_per_launch"],
+                    "traffic_source": None if tr is None else tr["source"], "peak_source": pk["source"],
+                    "algo_bytes_per_elem": BYTES[dom], "algo_bytes_per_launch": BYTES[dom] * n_local,
+                    "ms_per_launch": t}
     cpu = None
     if world == 1 and not args.no_cpu:
         rows_cpu = oracle_rows_for(cfg, args.cpu_seconds)

@@ -1,4 +1,7 @@
-for h in 0 1 2 3; do
-KVQ_TC_HINTS=$h timeout 400 python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_h$h.log 2>&1; echo "hints=$h"; tail -1 gpurun_out/bench_h$h.log | grep -o '"roundtrip": {"ms": [0-9.]*'
-KVQ_TC_HINTS=$h ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:attn_tc_kernel -s 1 -c 1 python bench.py --config C4 --steps 1 --warmup 3 --no-e2e --no-cpu --no-pass-events 2>&1 | grep -E "dram__bytes|duration"
-done
+# round-1 official artefacts: bench line, ncu launch list, ncu --set full of the hot kernels
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
+python bench.py > gpurun_out/bench_r01.json 2> gpurun_out/bench_r01.err; tail -1 gpurun_out/bench_r01.json
+python bench.py --pipeline separate --no-e2e --no-cpu > gpurun_out/bench_r01_separate.json 2>&1; tail -1 gpurun_out/bench_r01_separate.json | cut -c1-300
+ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches_r01.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"attn_tc_kernel|colmax_v4" -s 6 -c 2 -o gpurun_out/full_r01 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_full_r01.log 2>&1
+tail -2 gpurun_out/ncu_full_r01.log
