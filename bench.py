@@ -179,7 +179,9 @@ def run_kvq(args, cfg, rank, world, local_rank):
     kvq.kvq_device_check()
     T, D, nq = cfg["T"], cfg["D"], cfg["nq"]
     row0, rows = shard_rows(T, world, rank)
-    comm = make_comm(rank, world) if world > 1 else None
+    # Under torchrun (even with one process) the NCCL exchange path is exercised:
+    # kvq_compute_scales all-reduces the column maxima, the metrics their partials.
+    comm = make_comm(rank, world) if dist.is_available() and dist.is_initialized() else None
     stream = torch.cuda.current_stream()
 
     # device-resident inputs (generated on the GPU by the seeded counter RNG; rank r makes its rows)
@@ -290,6 +292,8 @@ def run_kvq(args, cfg, rank, world, local_rank):
                "steps": e2e_steps, "api": "kvq_roundtrip_host (pinned host K/Q -> scales, codes, metrics)",
                "attn_mean_abs": r["metrics"]["attn_mean_abs"]}
 
+    if comm is not None:
+        comm.destroy()
     if rank != 0:
         return
     value = T * D / (ms * 1e-3)
@@ -324,7 +328,7 @@ def run_kvq(args, cfg, rank, world, local_rank):
                    "pipeline": args.pipeline,
                    "l2_flush": "none needed: inputs larger than L2 (K alone is %.2f GB > 126 MB)" % (4 * T * D / 1e9)
                    if 4 * T * D > 2 * 126e6 else "inputs L2-resident (warm)",
-                   "parallelism": f"token-shard x{world}"},
+                   "parallelism": f"token-shard x{world}", "comm": "nccl (libkvq kvq_comm_t)" if comm else None},
         "hbm": {"GBps": algo_bytes / (ms * 1e-3) / 1e9 / world, "algo_bytes_per_elem": algo_per_elem,
                 "frac_of_peak_per_gpu": algo_bytes / (ms * 1e-3) / 1e9 / world / pk["hbm_gbs"]},
         "passes": pass_report, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
@@ -356,7 +360,8 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return
-    if world > 1:
+    launched = "WORLD_SIZE" in os.environ  # torchrun / torch.distributed.run
+    if launched:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
@@ -364,7 +369,7 @@ def main():
     try:
         run_kvq(args, cfg, rank, world, local_rank)
     finally:
-        if world > 1:
+        if launched:
             import torch.distributed as dist
             dist.destroy_process_group()
 

@@ -108,6 +108,19 @@ kvq_status kvq_dequantize(const int8_t *Kq, const float *scales, int64_t T, int6
 kvq_status kvq_quantize_dequantize(const float *K, const float *scales, int64_t T, int64_t D,
                                    int8_t *Kq, float *K_hat, void *stream);
 
+/* a1+a2+a3+a4 in ONE cooperative launch (single GPU, D % 4 == 0, aligned): the
+ * column max pass pulls K into the 126 MB L2, a grid-wide barrier, then each
+ * thread forms its own columns' scales and quantizes + dequantizes the same
+ * elements (from L2 when K fits).  Results are bit-identical to
+ * kvq_compute_scales + kvq_quantize_dequantize, which is what runs otherwise
+ * (comm != NULL, unaligned, or no co-resident grid).  workspace: device scratch
+ * of kvq_quantize_fused_workspace_size(T, D) bytes.  *single_pass_out [host,
+ * nullable] reports which path ran. */
+size_t kvq_quantize_fused_workspace_size(int64_t T, int64_t D);
+kvq_status kvq_quantize_fused(const float *K, int64_t T, int64_t D, float *scales, int8_t *Kq,
+                              float *K_hat, void *workspace, size_t workspace_bytes, kvq_comm_t comm,
+                              int *single_pass_out, void *stream);
+
 /* a5+a6: the paper's fidelity checks.
  * K, K_hat: [T][D] float32 in.  Q: [nq][D] float32 queries or NULL (nq == 0).
  * scales: [D] or NULL (only used for theoretical_max).  workspace: device

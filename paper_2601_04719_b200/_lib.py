@@ -42,6 +42,8 @@ SIGNATURES = {
     "kvq_quantize": (_int, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "kvq_dequantize": (_int, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "kvq_quantize_dequantize": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "kvq_quantize_fused_workspace_size": (_sz, [_i64, _i64]),
+    "kvq_quantize_fused": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp, ctypes.POINTER(_int), _vp]),
     "kvq_error_metrics_workspace_size": (_sz, [_i64, _i64, _i64]),
     "kvq_error_metrics_async": (_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _sz, _vp, _vp, _vp]),
     "kvq_error_metrics": (_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _sz, _vp,

@@ -180,6 +180,40 @@ extern "C" kvq_status kvq_dequantize(const int8_t *Kq, const float *scales, int6
     return launch_dequantize(Kq, scales, T, D, K_hat, (cudaStream_t)stream);
 }
 
+// ------------------------------------------------------------------------------ a1..a4 in one launch
+extern "C" size_t kvq_quantize_fused_workspace_size(int64_t T, int64_t D) {
+    if (bad_dims(T, D)) return 0;
+    return single_pass_workspace_size(D);
+}
+
+extern "C" kvq_status kvq_quantize_fused(const float *K, int64_t T, int64_t D, float *scales, int8_t *Kq,
+                                         float *K_hat, void *workspace, size_t workspace_bytes, kvq_comm_t comm,
+                                         int *single_pass_out, void *stream) {
+    KVQ_REQUIRE(K && scales && Kq && K_hat && workspace, "kvq_quantize_fused: NULL pointer");
+    KVQ_REQUIRE(!bad_dims(T, D), "kvq_quantize_fused: need T >= 1, D >= 1, T*D <= 2^62");
+    KVQ_REQUIRE(workspace_bytes >= single_pass_workspace_size(D), "kvq_quantize_fused: workspace too small");
+    const size_t n = (size_t)(T * D);
+    KVQ_REQUIRE(!overlap(K, n * 4, Kq, n) && !overlap(K_hat, n * 4, K, n * 4) && !overlap(K_hat, n * 4, Kq, n) &&
+                    !overlap(scales, (size_t)D * 4, K, n * 4) && !overlap(scales, (size_t)D * 4, Kq, n) &&
+                    !overlap(scales, (size_t)D * 4, K_hat, n * 4) &&
+                    !overlap(workspace, workspace_bytes, K, n * 4),
+                "kvq_quantize_fused: buffers alias");
+    KVQ_TRY(device_ok());
+    cudaStream_t s = (cudaStream_t)stream;
+    if (single_pass_out) *single_pass_out = 0;
+    if (!comm) {
+        kvq_status st = launch_single_pass(K, T, D, scales, Kq, K_hat, workspace, s);
+        if (st == KVQ_OK) {
+            if (single_pass_out) *single_pass_out = 1;
+            return KVQ_OK;
+        }
+        if (st != KVQ_ERR_UNSUPPORTED) return st;
+    }
+    // two passes (sharded input, too large for one co-resident grid, or unaligned)
+    KVQ_TRY(kvq_compute_scales(K, T, D, scales, comm, stream));
+    return launch_quantize(K, scales, T, D, Kq, K_hat, s);
+}
+
 // ------------------------------------------------------------------------------ a5 + a6
 extern "C" size_t kvq_error_metrics_workspace_size(int64_t T, int64_t D, int64_t nq) {
     if (bad_dims(T, D) || nq < 0) return 0;

@@ -43,6 +43,10 @@ kvq_status launch_quantize(const float *K, const float *scales, int64_t T, int64
 kvq_status launch_dequantize(const int8_t *Kq, const float *scales, int64_t T, int64_t D, float *K_hat,
                              cudaStream_t s);
 
+size_t single_pass_workspace_size(int64_t D);
+kvq_status launch_single_pass(const float *K, int64_t T, int64_t D, float *scales, int8_t *Kq, float *K_hat,
+                              void *ws, cudaStream_t s);
+
 // ---- metrics kernels (metrics_kernels.cu, attn_tc.cu)
 // Writes per-rank totals {sum_sq, attn_abs_sum, n_elems, n_scores} (double[4]) and
 // {max_abs_bits, theo_max_bits} (uint64[2]) into the workspace tail; returns

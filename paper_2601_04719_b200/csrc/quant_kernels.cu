@@ -16,6 +16,7 @@
 //    idea with stride a multiple of D) handles D % 4 != 0 or misaligned bases,
 //    which the paper's vectorized kernel leaves unwritten.
 #include <algorithm>
+#include <string>
 
 #include "device_common.cuh"
 #include "kvq_internal.h"
@@ -249,6 +250,109 @@ __global__ void __launch_bounds__(kThreads) dequant_scalar_kernel(const int8_t *
     }
 }
 
+// ============================================================================ a1+a2+a3+a4 single pass
+// One cooperative launch for L2-resident sizes: phase 1 is the column abs-max of
+// colmax_v4_kernel, then a grid-wide barrier, then each thread forms the scales of
+// its own 4 columns (Eq. 6, IEEE division) and runs the fused quantize+dequantize
+// loop of quant_v4_kernel over the same elements, which the first phase has just
+// pulled into the 126 MB L2.  Same geometry in both phases (column-owning threads).
+__device__ __forceinline__ void grid_barrier_once(unsigned *ctr, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        while (*reinterpret_cast<volatile unsigned *>(ctr) < nblocks) __nanosleep(64);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int U>
+__global__ void __launch_bounds__(kThreads) single_pass_v4_kernel(const float4 *__restrict__ K, int64_t n4,
+                                                                  int64_t cols4, int64_t G, uint32_t *mbits,
+                                                                  unsigned *barrier, float *__restrict__ scales,
+                                                                  uint32_t *__restrict__ Kq4,
+                                                                  float4 *__restrict__ Kh4) {
+    extern __shared__ uint32_t smax[];  // [4*cols4] when cols4 <= kThreads
+    const bool share = cols4 <= kThreads;
+    const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    const int64_t c4 = g < G ? g % cols4 : 0;
+    // ---- phase 1: a1 (colmax_v4_kernel)
+    if (share) {
+        for (int i = threadIdx.x; i < 4 * cols4; i += kThreads) smax[i] = 0u;
+        __syncthreads();
+    }
+    uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+    if (g < G) {
+        int64_t i = g;
+        for (; i + (U - 1) * G < n4; i += U * G) {
+            float4 v[U];
+#pragma unroll
+            for (int k = 0; k < U; k++) v[k] = __ldcg(K + i + k * G);  // keep K in L2 for phase 2
+#pragma unroll
+            for (int k = 0; k < U; k++) {
+                m0 = max(m0, absbits(v[k].x));
+                m1 = max(m1, absbits(v[k].y));
+                m2 = max(m2, absbits(v[k].z));
+                m3 = max(m3, absbits(v[k].w));
+            }
+        }
+        for (; i < n4; i += G) {
+            float4 v = __ldcg(K + i);
+            m0 = max(m0, absbits(v.x));
+            m1 = max(m1, absbits(v.y));
+            m2 = max(m2, absbits(v.z));
+            m3 = max(m3, absbits(v.w));
+        }
+    }
+    if (share) {
+        if (g < G) {
+            atomicMax(&smax[4 * c4 + 0], m0);
+            atomicMax(&smax[4 * c4 + 1], m1);
+            atomicMax(&smax[4 * c4 + 2], m2);
+            atomicMax(&smax[4 * c4 + 3], m3);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < 4 * cols4; i += kThreads)
+            if (smax[i]) atomicMax(&mbits[i], smax[i]);
+    } else if (g < G) {
+        atomicMax(&mbits[4 * c4 + 0], m0);
+        atomicMax(&mbits[4 * c4 + 1], m1);
+        atomicMax(&mbits[4 * c4 + 2], m2);
+        atomicMax(&mbits[4 * c4 + 3], m3);
+    }
+    grid_barrier_once(barrier, gridDim.x);
+    if (g >= G) return;
+    // ---- a2 for the thread's own columns (Eq. 6), published by the threads of row-lane 0
+    float sc[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) sc[j] = __fdiv_rn(__uint_as_float(__ldcg(mbits + 4 * c4 + j)), 127.0f);
+    if (g < cols4) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) scales[4 * c4 + j] = sc[j];
+    }
+    // ---- phase 2: a3 + a4 (quant_v4_kernel<.., true>)
+    const ColQ q0 = make_colq(sc[0]), q1 = make_colq(sc[1]), q2 = make_colq(sc[2]), q3 = make_colq(sc[3]);
+    const bool col_exact = q0.exact | q1.exact | q2.exact | q3.exact;
+    for (int64_t i = g; i < n4; i += 4 * G) {
+        float4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+            if (i + k * G < n4) v[k] = __ldcs(K + i + k * G);  // last use: evict
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int64_t idx = i + k * G;
+            if (idx < n4) {
+                uint32_t w;
+                float4 xh;
+                quant4<true>(v[k], q0, q1, q2, q3, col_exact, w, xh);
+                Kq4[idx] = w;
+                Kh4[idx] = xh;
+            }
+        }
+    }
+}
+
 // ============================================================================ host launchers
 static inline bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
@@ -343,6 +447,49 @@ kvq_status launch_dequantize(const int8_t *Kq, const float *scales, int64_t T, i
         dequant_scalar_kernel<kUDequant><<<p.blocks, kThreads, 0, s>>>(Kq, scales, K_hat, n, D, p.G);
     }
     return check_launch("dequantize");
+}
+
+}  // namespace kvq
+
+namespace kvq {
+
+size_t single_pass_workspace_size(int64_t D) { return (size_t)D * 4 + 256; }
+
+// Returns KVQ_ERR_UNSUPPORTED (nothing launched) when the shape or alignment does
+// not allow the single cooperative pass; the caller then runs the two passes.
+kvq_status launch_single_pass(const float *K, int64_t T, int64_t D, float *scales, int8_t *Kq, float *K_hat,
+                              void *ws, cudaStream_t s) {
+    if (D % 4 || !aligned(K, 16) || !aligned(Kq, 4) || !aligned(K_hat, 16))
+        return KVQ_ERR_UNSUPPORTED;
+    const int64_t cols4 = D / 4;
+    if (cols4 > (int64_t)device_info().num_sms * kThreads) return KVQ_ERR_UNSUPPORTED;
+    const size_t smem = cols4 <= kThreads ? (size_t)4 * cols4 * sizeof(uint32_t) : 0;
+    static int nb_per_sm = [] {
+        int nb = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, single_pass_v4_kernel<kUColmax>, kThreads,
+                                                      4 * kThreads * sizeof(uint32_t));
+        cudaGetLastError();
+        return nb;
+    }();
+    if (nb_per_sm < 1) return KVQ_ERR_UNSUPPORTED;
+    StreamPlan p = plan_stream(T, cols4, nb_per_sm * kThreads);
+    if ((int64_t)p.blocks > (int64_t)nb_per_sm * device_info().num_sms) return KVQ_ERR_UNSUPPORTED;
+    uint32_t *mbits = reinterpret_cast<uint32_t *>((reinterpret_cast<uintptr_t>(ws) + 255) & ~(uintptr_t)255);
+    unsigned *bar = reinterpret_cast<unsigned *>(mbits + D);
+    if (cudaMemsetAsync(mbits, 0, (size_t)D * 4 + 64, s) != cudaSuccess) return check_launch("single_pass memset");
+    const float4 *K4 = reinterpret_cast<const float4 *>(K);
+    int64_t n4 = T * D / 4, G = p.G;
+    uint32_t *Q4 = reinterpret_cast<uint32_t *>(Kq);
+    float4 *H4 = reinterpret_cast<float4 *>(K_hat);
+    void *args[] = {(void *)&K4, (void *)&n4, (void *)&cols4, (void *)&G, (void *)&mbits, (void *)&bar,
+                    (void *)&scales, (void *)&Q4, (void *)&H4};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void *)single_pass_v4_kernel<kUColmax>, dim3(p.blocks),
+                                                dim3(kThreads), args, smem, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(KVQ_ERR_CUDA, std::string("single_pass cooperative launch: ") + cudaGetErrorString(e));
+    }
+    return KVQ_OK;
 }
 
 }  // namespace kvq

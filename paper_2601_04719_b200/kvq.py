@@ -18,6 +18,7 @@ __all__ = [
     "kvq_error_metrics", "kvq_error_metrics_async", "kvq_error_metrics_workspace_size", "kvq_attention_scores",
     "kvq_roundtrip_host", "kvq_roundtrip_host_workspace_size", "kvq_synth_fill", "kvq_device_check",
     "kvq_comm_unique_id", "METRICS_BYTES", "metrics_from_device", "kvq_roundtrip", "kvq_roundtrip_workspace_size",
+    "kvq_quantize_fused",
 ]
 
 load()  # fail loudly at import if libkvq.so cannot be loaded or built
@@ -135,6 +136,28 @@ def kvq_quantize_dequantize(K: torch.Tensor, scales: torch.Tensor, Kq: Optional[
     check(load().kvq_quantize_dequantize(_ptr(K), _ptr(scales), T, D, _ptr(Kq), _ptr(K_hat), _stream(stream)),
           "kvq_quantize_dequantize")
     return Kq, K_hat
+
+
+def kvq_quantize_fused(K: torch.Tensor, scales: Optional[torch.Tensor] = None, Kq: Optional[torch.Tensor] = None,
+                       K_hat: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                       comm: Optional[Comm] = None, stream=None):
+    """a1..a4 in one cooperative launch when possible.  Returns (scales, Kq, K_hat, single_pass)."""
+    T, D = _mat(K, torch.float32, "K")
+    if scales is None:
+        scales = torch.empty(D, dtype=torch.float32, device=K.device)
+    _vec(scales, D, "scales")
+    if Kq is None:
+        Kq = torch.empty((T, D), dtype=torch.int8, device=K.device)
+    if K_hat is None:
+        K_hat = torch.empty((T, D), dtype=torch.float32, device=K.device)
+    need = int(load().kvq_quantize_fused_workspace_size(T, D))
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=K.device)
+    flag = ctypes.c_int(0)
+    check(load().kvq_quantize_fused(_ptr(K), T, D, _ptr(scales), _ptr(Kq), _ptr(K_hat), _ptr(workspace),
+                                    workspace.numel(), _comm_handle(comm), ctypes.byref(flag), _stream(stream)),
+          "kvq_quantize_fused")
+    return scales, Kq, K_hat, bool(flag.value)
 
 
 def kvq_error_metrics_workspace_size(T: int, D: int, nq: int) -> int:

@@ -456,3 +456,35 @@ def test_roundtrip_matches_separate_calls_C2(kvq, orc):
     assert m1["max_abs"] == m2["max_abs"]
     for k in ("l2", "attn_mean_abs"):
         assert _rel(m2[k], m1[k]) <= REL
+
+
+# ----------------------------------------------------------------------------- single cooperative pass (C5)
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("T,D,expect_single", [(1, 4, True), (1000, 128, True), (8192, 1024, True),
+                                               (333, 8192, True), (77, 13, False), (4096, 4, True),
+                                               (1 << 20, 128, True)])
+def test_quantize_fused_single_pass(kvq, orc, T, D, expect_single):
+    K = orc.fill(T, D, 12, 1)
+    s, q, kh, single = kvq.kvq_quantize_fused(dev(K))
+    assert single == expect_single
+    so, qo, kho = orc.roundtrip(K)
+    same_bits(host(s), so)
+    same_bits(host(q), qo)
+    same_bits(host(kh), kho)
+
+
+@pytest.mark.timeout(300)
+def test_quantize_fused_repeat_and_special_columns(kvq, orc):
+    """Workspace reuse across calls (counter/bits re-zeroed), zero and subnormal columns."""
+    rng = np.random.default_rng(4)
+    K = rng.uniform(-1, 1, (2048, 64)).astype(np.float32)
+    K[:, 3] = 0.0
+    K[:, 7] *= np.float32(2.0 ** -140)
+    ws = torch.empty(kvq.load().kvq_quantize_fused_workspace_size(2048, 64), dtype=torch.uint8, device="cuda")
+    so, qo, kho = orc.roundtrip(K)
+    for _ in range(3):
+        s, q, kh, single = kvq.kvq_quantize_fused(dev(K), workspace=ws)
+        assert single
+        same_bits(host(s), so)
+        same_bits(host(q), qo)
+        same_bits(host(kh), kho)
