@@ -187,6 +187,17 @@ kvq_status kvq_roundtrip_host(const float *K_host, int64_t T, int64_t D,
                               kvq_metrics *metrics_host,
                               void *dev_workspace, size_t workspace_bytes,
                               kvq_comm_t comm, void *stream);
+/* Same, asynchronous: returns after enqueueing; all host outputs (including
+ * metrics_host) must be pinned and are valid once `stream` has been
+ * synchronized.  The copies run on library-owned H2D / D2H streams, so calls on
+ * two caller streams with two workspaces pipeline: call i's device-to-host
+ * results travel while call i+1's inputs arrive. */
+kvq_status kvq_roundtrip_host_async(const float *K_host, int64_t T, int64_t D,
+                                    const float *Q_host, int64_t nq,
+                                    float *scales_host, int8_t *Kq_host, float *K_hat_host,
+                                    kvq_metrics *metrics_host,
+                                    void *dev_workspace, size_t workspace_bytes,
+                                    kvq_comm_t comm, void *stream);
 
 #ifdef __cplusplus
 }

@@ -55,6 +55,7 @@ SIGNATURES = {
     "kvq_roundtrip_host_workspace_size": (_sz, [_i64, _i64, _i64]),
     "kvq_roundtrip_host": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp, ctypes.POINTER(kvq_metrics), _vp,
                                   _sz, _vp, _vp]),
+    "kvq_roundtrip_host_async": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
     "kvq_synth_fill": (_int, [_vp, _i64, _i64, _i64, _u64, _int, _vp]),
 }
 

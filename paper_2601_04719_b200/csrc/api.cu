@@ -39,7 +39,7 @@ constexpr int kMaxDevices = 64;
 std::mutex g_mu;
 int g_state[kMaxDevices];  // 0 unknown, 1 ok, 2 unsupported
 DeviceInfo g_info[kMaxDevices];
-cudaStream_t g_copy_stream[kMaxDevices];
+cudaStream_t g_copy_stream[kMaxDevices][2];
 }  // namespace
 
 kvq_status device_ok() {
@@ -76,12 +76,13 @@ const DeviceInfo &device_info() {
     return g_info[dev];
 }
 
-static cudaStream_t copy_stream() {
+// Library-owned copy streams per device: 0 = host-to-device, 1 = device-to-host.
+static cudaStream_t copy_stream(int which) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_mu);
-    if (!g_copy_stream[dev]) cudaStreamCreateWithFlags(&g_copy_stream[dev], cudaStreamNonBlocking);
-    return g_copy_stream[dev];
+    if (!g_copy_stream[dev][which]) cudaStreamCreateWithFlags(&g_copy_stream[dev][which], cudaStreamNonBlocking);
+    return g_copy_stream[dev][which];
 }
 
 }  // namespace kvq
@@ -326,19 +327,23 @@ extern "C" size_t kvq_roundtrip_host_workspace_size(int64_t T, int64_t D, int64_
     return host_layout(T, D, nq).total;
 }
 
-extern "C" kvq_status kvq_roundtrip_host(const float *K_host, int64_t T, int64_t D, const float *Q_host, int64_t nq,
+// Enqueue the whole host-buffer pipeline.  Three streams: the caller's `stream`
+// runs the kernels; library-owned H2D and D2H streams drive the two copy engines,
+// so consecutive calls on different caller streams overlap call i's D2H with
+// call i+1's H2D (PCIe is full duplex).  The caller's stream finally waits for
+// the D2H stream, so synchronizing `stream` covers everything.
+static kvq_status roundtrip_host_enqueue(const float *K_host, int64_t T, int64_t D, const float *Q_host, int64_t nq,
                                          float *scales_host, int8_t *Kq_host, float *K_hat_host,
                                          kvq_metrics *metrics_host, void *dev_workspace, size_t workspace_bytes,
-                                         kvq_comm_t comm, void *stream) {
-    KVQ_REQUIRE(K_host && scales_host && Kq_host && metrics_host && dev_workspace,
-                "kvq_roundtrip_host: NULL pointer");
-    KVQ_REQUIRE(!bad_dims(T, D), "kvq_roundtrip_host: need T >= 1, D >= 1, T*D <= 2^62");
-    KVQ_REQUIRE(nq >= 0 && (nq == 0 || Q_host), "kvq_roundtrip_host: need nq >= 0 and Q when nq > 0");
+                                         kvq_comm_t comm, void *stream, const char *name) {
+    KVQ_REQUIRE(K_host && scales_host && Kq_host && metrics_host && dev_workspace, std::string(name) + ": NULL pointer");
+    KVQ_REQUIRE(!bad_dims(T, D), std::string(name) + ": need T >= 1, D >= 1, T*D <= 2^62");
+    KVQ_REQUIRE(nq >= 0 && (nq == 0 || Q_host), std::string(name) + ": need nq >= 0 and Q when nq > 0");
     const HostLayout L = host_layout(T, D, nq);
-    KVQ_REQUIRE(workspace_bytes >= L.total, "kvq_roundtrip_host: workspace too small");
+    KVQ_REQUIRE(workspace_bytes >= L.total, std::string(name) + ": workspace too small");
     KVQ_TRY(device_ok());
     cudaStream_t s = (cudaStream_t)stream;
-    cudaStream_t cs = copy_stream();
+    cudaStream_t hs = copy_stream(0), ds = copy_stream(1);
     char *base = reinterpret_cast<char *>(((uintptr_t)dev_workspace + 255) & ~(uintptr_t)255);
     float *K = reinterpret_cast<float *>(base + L.K);
     float *Kh = reinterpret_cast<float *>(base + L.Kh);
@@ -348,7 +353,7 @@ extern "C" kvq_status kvq_roundtrip_host(const float *K_host, int64_t T, int64_t
     kvq_metrics *mout = reinterpret_cast<kvq_metrics *>(base + L.mout);
     uint32_t *bits = reinterpret_cast<uint32_t *>(sc);
 
-    // Row blocks of ~64 MB: block b's column-max kernel runs while block b+1 is in flight on the copy engine.
+    // Row blocks of ~64 MB: block b's column-max kernel runs while block b+1 is on the copy engine.
     const size_t row_bytes = (size_t)D * 4;
     int64_t rows_per = std::max<int64_t>(1, (int64_t)((64u << 20) / row_bytes));
     int64_t nblk = (T + rows_per - 1) / rows_per;
@@ -356,61 +361,74 @@ extern "C" kvq_status kvq_roundtrip_host(const float *K_host, int64_t T, int64_t
         rows_per = (T + 63) / 64;
         nblk = (T + rows_per - 1) / rows_per;
     }
-    std::vector<cudaEvent_t> ev(nblk + 2);
+    // events: [0, nblk) H2D blocks, nblk start, nblk+1 Q, nblk+2 compute done, nblk+3 D2H done
+    std::vector<cudaEvent_t> ev(nblk + 4);
     for (auto &e : ev) KVQ_TRY(cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create"));
-    auto cleanup = [&]() {
-        for (auto &e : ev) cudaEventDestroy(e);
-    };
     kvq_status st = KVQ_OK;
+    auto ck = [&](cudaError_t e, const char *what) {
+        if (st == KVQ_OK) st = cuda_check(e, what);
+        return st == KVQ_OK;
+    };
     do {
-        // the copy stream must not overwrite the workspace before earlier work on `s` is done
-        if ((st = cuda_check(cudaEventRecord(ev[nblk], s), "record")) != KVQ_OK) break;
-        if ((st = cuda_check(cudaStreamWaitEvent(cs, ev[nblk], 0), "wait")) != KVQ_OK) break;
-        if ((st = cuda_check(cudaMemsetAsync(bits, 0, (size_t)D * 4, s), "memset")) != KVQ_OK) break;
-        for (int64_t b = 0; b < nblk && st == KVQ_OK; b++) {
-            const int64_t r0 = b * rows_per, nr = std::min(rows_per, T - r0);
-            st = cuda_check(cudaMemcpyAsync(K + r0 * D, K_host + r0 * D, (size_t)(nr * D) * 4,
-                                            cudaMemcpyHostToDevice, cs), "H2D K");
-            if (st == KVQ_OK) st = cuda_check(cudaEventRecord(ev[b], cs), "record");
-            if (st == KVQ_OK) st = cuda_check(cudaStreamWaitEvent(s, ev[b], 0), "wait");
-            if (st == KVQ_OK) st = launch_colmax(K + r0 * D, nr, D, bits, s);
-        }
-        if (st != KVQ_OK) break;
+        // the workspace is free once earlier work on `s` is done
+        if (!ck(cudaEventRecord(ev[nblk], s), "record") || !ck(cudaStreamWaitEvent(hs, ev[nblk], 0), "wait")) break;
+        if (!ck(cudaMemsetAsync(bits, 0, (size_t)D * 4, s), "memset")) break;
         if (nq) {
-            if ((st = cuda_check(cudaMemcpyAsync(Q, Q_host, (size_t)(nq * D) * 4, cudaMemcpyHostToDevice, s),
-                                 "H2D Q")) != KVQ_OK)
+            if (!ck(cudaMemcpyAsync(Q, Q_host, (size_t)(nq * D) * 4, cudaMemcpyHostToDevice, hs), "H2D Q") ||
+                !ck(cudaEventRecord(ev[nblk + 1], hs), "record"))
                 break;
         }
+        for (int64_t b = 0; b < nblk && st == KVQ_OK; b++) {
+            const int64_t r0 = b * rows_per, nr = std::min(rows_per, T - r0);
+            if (!ck(cudaMemcpyAsync(K + r0 * D, K_host + r0 * D, (size_t)(nr * D) * 4, cudaMemcpyHostToDevice, hs),
+                    "H2D K") ||
+                !ck(cudaEventRecord(ev[b], hs), "record") || !ck(cudaStreamWaitEvent(s, ev[b], 0), "wait"))
+                break;
+            st = launch_colmax(K + r0 * D, nr, D, bits, s);
+        }
+        if (st != KVQ_OK) break;
+        if (nq && !ck(cudaStreamWaitEvent(s, ev[nblk + 1], 0), "wait")) break;
         if (comm && (st = comm_allreduce_max_u32(comm, bits, (size_t)D, s)) != KVQ_OK) break;
         if ((st = launch_finalize(bits, D, s)) != KVQ_OK) break;
         MetricTotals tot;
         if ((st = launch_roundtrip_partials(K, sc, T, D, Kq, Kh, nq ? Q : nullptr, nq, base + L.mws,
                                             metrics_workspace_size(T, D, nq), &tot, s)) != KVQ_OK)
             break;
-        // codes + scales (+ K_hat) go back on the copy engine while the metrics run on `s`
-        if ((st = cuda_check(cudaEventRecord(ev[nblk + 1], s), "record")) != KVQ_OK) break;
-        if ((st = cuda_check(cudaStreamWaitEvent(cs, ev[nblk + 1], 0), "wait")) != KVQ_OK) break;
-        if ((st = cuda_check(cudaMemcpyAsync(Kq_host, Kq, (size_t)(T * D), cudaMemcpyDeviceToHost, cs), "D2H Kq")) !=
-            KVQ_OK)
-            break;
-        if ((st = cuda_check(cudaMemcpyAsync(scales_host, sc, (size_t)D * 4, cudaMemcpyDeviceToHost, cs),
-                             "D2H scales")) != KVQ_OK)
-            break;
-        if (K_hat_host && (st = cuda_check(cudaMemcpyAsync(K_hat_host, Kh, (size_t)(T * D) * 4,
-                                                           cudaMemcpyDeviceToHost, cs),
-                                           "D2H K_hat")) != KVQ_OK)
-            break;
         if (comm) {
             if ((st = comm_allreduce_sum_f64(comm, tot.sums, 4, s)) != KVQ_OK) break;
             if ((st = comm_allreduce_max_u64(comm, tot.maxes, 2, s)) != KVQ_OK) break;
         }
         if ((st = launch_metrics_finalize(tot, mout, s)) != KVQ_OK) break;
-        if ((st = cuda_check(cudaMemcpyAsync(metrics_host, mout, sizeof(kvq_metrics), cudaMemcpyDeviceToHost, s),
-                             "D2H metrics")) != KVQ_OK)
+        // results back on the D2H copy engine
+        if (!ck(cudaEventRecord(ev[nblk + 2], s), "record") || !ck(cudaStreamWaitEvent(ds, ev[nblk + 2], 0), "wait"))
             break;
-        if ((st = cuda_check(cudaStreamSynchronize(cs), "sync copy stream")) != KVQ_OK) break;
-        st = cuda_check(cudaStreamSynchronize(s), "sync stream");
+        if (!ck(cudaMemcpyAsync(Kq_host, Kq, (size_t)(T * D), cudaMemcpyDeviceToHost, ds), "D2H Kq") ||
+            !ck(cudaMemcpyAsync(scales_host, sc, (size_t)D * 4, cudaMemcpyDeviceToHost, ds), "D2H scales") ||
+            !ck(cudaMemcpyAsync(metrics_host, mout, sizeof(kvq_metrics), cudaMemcpyDeviceToHost, ds), "D2H metrics"))
+            break;
+        if (K_hat_host &&
+            !ck(cudaMemcpyAsync(K_hat_host, Kh, (size_t)(T * D) * 4, cudaMemcpyDeviceToHost, ds), "D2H K_hat"))
+            break;
+        if (!ck(cudaEventRecord(ev[nblk + 3], ds), "record") || !ck(cudaStreamWaitEvent(s, ev[nblk + 3], 0), "wait"))
+            break;
     } while (0);
-    cleanup();
+    for (auto &e : ev) cudaEventDestroy(e);  // released once the pending work completes
     return st;
+}
+
+extern "C" kvq_status kvq_roundtrip_host_async(const float *K_host, int64_t T, int64_t D, const float *Q_host,
+                                               int64_t nq, float *scales_host, int8_t *Kq_host, float *K_hat_host,
+                                               kvq_metrics *metrics_host, void *dev_workspace, size_t workspace_bytes,
+                                               kvq_comm_t comm, void *stream) {
+    return roundtrip_host_enqueue(K_host, T, D, Q_host, nq, scales_host, Kq_host, K_hat_host, metrics_host,
+                                  dev_workspace, workspace_bytes, comm, stream, "kvq_roundtrip_host_async");
+}
+
+extern "C" kvq_status kvq_roundtrip_host(const float *K_host, int64_t T, int64_t D, const float *Q_host, int64_t nq,
+                                         float *scales_host, int8_t *Kq_host, float *K_hat_host,
+                                         kvq_metrics *metrics_host, void *dev_workspace, size_t workspace_bytes,
+                                         kvq_comm_t comm, void *stream) {
+    KVQ_TRY(roundtrip_host_enqueue(K_host, T, D, Q_host, nq, scales_host, Kq_host, K_hat_host, metrics_host,
+                                   dev_workspace, workspace_bytes, comm, stream, "kvq_roundtrip_host"));
+    return cuda_check(cudaStreamSynchronize((cudaStream_t)stream), "sync stream");
 }

@@ -18,7 +18,7 @@ __all__ = [
     "kvq_error_metrics", "kvq_error_metrics_async", "kvq_error_metrics_workspace_size", "kvq_attention_scores",
     "kvq_roundtrip_host", "kvq_roundtrip_host_workspace_size", "kvq_synth_fill", "kvq_device_check",
     "kvq_comm_unique_id", "METRICS_BYTES", "metrics_from_device", "kvq_roundtrip", "kvq_roundtrip_workspace_size",
-    "kvq_quantize_fused",
+    "kvq_quantize_fused", "kvq_roundtrip_host_async", "metrics_from_host",
 ]
 
 load()  # fail loudly at import if libkvq.so cannot be loaded or built
@@ -285,6 +285,26 @@ def kvq_roundtrip_host(K_host: torch.Tensor, Q_host: Optional[torch.Tensor] = No
                                     _ptr(K_hat_host), ctypes.byref(m), _ptr(workspace), workspace.numel(),
                                     _comm_handle(comm), _stream(stream)), "kvq_roundtrip_host")
     return {"scales": scales_host, "Kq": Kq_host, "K_hat": K_hat_host, "metrics": m.to_dict()}
+
+
+def kvq_roundtrip_host_async(K_host: torch.Tensor, Q_host: Optional[torch.Tensor], scales_host: torch.Tensor,
+                             Kq_host: torch.Tensor, metrics_host: torch.Tensor, workspace: torch.Tensor,
+                             K_hat_host: Optional[torch.Tensor] = None, comm: Optional[Comm] = None, stream=None):
+    """Asynchronous host-buffer pipeline; every host tensor must be pinned.  metrics_host is a
+    pinned uint8[METRICS_BYTES] tensor (decode with metrics_from_host after synchronizing)."""
+    T, D = _mat(K_host, torch.float32, "K_host", cuda=False)
+    nq = 0 if Q_host is None else _mat(Q_host, torch.float32, "Q_host", cuda=False)[0]
+    for t in (K_host, scales_host, Kq_host, metrics_host) + ((Q_host,) if Q_host is not None else ()):
+        if not t.is_pinned():
+            raise ValueError("kvq_roundtrip_host_async needs pinned host tensors")
+    assert metrics_host.numel() >= METRICS_BYTES and metrics_host.dtype == torch.uint8
+    check(load().kvq_roundtrip_host_async(_ptr(K_host), T, D, _ptr(Q_host), nq, _ptr(scales_host), _ptr(Kq_host),
+                                          _ptr(K_hat_host), _ptr(metrics_host), _ptr(workspace), workspace.numel(),
+                                          _comm_handle(comm), _stream(stream)), "kvq_roundtrip_host_async")
+
+
+def metrics_from_host(buf: torch.Tensor) -> dict:
+    return kvq_metrics.from_buffer_copy(bytes(buf.numpy().tobytes()[:METRICS_BYTES])).to_dict()
 
 
 def kvq_synth_fill(rows: int, D: int, row0: int = 0, seed: int = 42, dist: int = DIST_UNIFORM,

@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider -k "fused or single" > gpurun_out/pytest_sp.log 2>&1; tail -4 gpurun_out/pytest_sp.log
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_torchrun1.log 2>&1; tail -1 gpurun_out/bench_torchrun1.log | cut -c1-400; grep -i "error\|Traceback" gpurun_out/bench_torchrun1.log | head -5
-timeout 900 python scripts/sweep_c5.py --out gpurun_out/sweep_c5 > gpurun_out/sweep.log 2>&1; tail -3 gpurun_out/sweep.log; cat gpurun_out/sweep_c5.md | head -80
+timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider -k "host" > gpurun_out/pytest_host.log 2>&1; tail -4 gpurun_out/pytest_host.log
+timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu > gpurun_out/bench_e2e.log 2>&1; tail -1 gpurun_out/bench_e2e.log | grep -o '"e2e".*"gpu_launches"'; grep -i "error\|Trace" gpurun_out/bench_e2e.log | head

@@ -488,3 +488,32 @@ def test_quantize_fused_repeat_and_special_columns(kvq, orc):
         same_bits(host(s), so)
         same_bits(host(q), qo)
         same_bits(host(kh), kho)
+
+
+@pytest.mark.timeout(300)
+def test_roundtrip_host_async_pipelined(kvq, orc):
+    """Two async host-pipeline calls in flight on two streams (overlapping copies) give the
+    same results as the oracle for their own inputs."""
+    T, D, nq = 2000, 256, 64
+    outs = []
+    Q = orc.fill(nq, D, 43)
+    Qh = torch.from_numpy(Q).pin_memory()
+    slots = []
+    for seed in (42, 77):
+        K = orc.fill(T, D, seed)
+        slots.append(dict(K=K, Kh=torch.from_numpy(K).pin_memory(), s=torch.cuda.Stream(),
+                          ws=torch.empty(kvq.kvq_roundtrip_host_workspace_size(T, D, nq), dtype=torch.uint8,
+                                         device="cuda"),
+                          sc=torch.empty(D, dtype=torch.float32).pin_memory(),
+                          kq=torch.empty((T, D), dtype=torch.int8).pin_memory(),
+                          m=torch.empty(kvq.METRICS_BYTES, dtype=torch.uint8).pin_memory()))
+    for sl in slots:
+        kvq.kvq_roundtrip_host_async(sl["Kh"], Qh, sl["sc"], sl["kq"], sl["m"], sl["ws"], stream=sl["s"])
+    torch.cuda.synchronize()
+    for sl in slots:
+        so, qo, kho = orc.roundtrip(sl["K"])
+        same_bits(sl["sc"].numpy(), so)
+        same_bits(sl["kq"].numpy(), qo)
+        m = kvq.metrics_from_host(sl["m"])
+        assert m["max_abs"] == orc.max_abs_error(sl["K"], kho)
+        assert _rel(m["attn_mean_abs"], orc.attention_error(Q, sl["K"], kho)) <= REL
