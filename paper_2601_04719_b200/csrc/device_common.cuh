@@ -101,6 +101,23 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint4 *p) {
     return r;
 }
 
+// Streaming (evict-first) stores for write-once outputs.
+__device__ __forceinline__ void st_cs_f4(float4 *p, float4 v) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void st_cs_u32(uint32_t *p, uint32_t v) {
+    asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+template <int SP>
+__device__ __forceinline__ void store_f4(float4 *p, float4 v) {
+    if (SP) st_cs_f4(p, v); else *p = v;
+}
+template <int SP>
+__device__ __forceinline__ void store_u32(uint32_t *p, uint32_t v) {
+    if (SP) st_cs_u32(p, v); else *p = v;
+}
+
 __device__ __forceinline__ uint32_t absbits(float x) { return __float_as_uint(x) & 0x7fffffffu; }
 
 // int8 code (as byte j of w) -> float, exact.
