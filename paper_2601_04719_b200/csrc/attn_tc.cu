@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nkb; kb++, g++) {
                     const int sk = g % KST;
-                    mbar_wait(&s.empty_k[sk], ((g / KST) & 1) ^ 1);
+                    mbar_wait_lazy(&s.empty_k[sk], ((g / KST) & 1) ^ 1);
                     mbar_arrive_tx(&s.full_k[sk], kbytes);
                     uint8_t *stg = s.buf + sk * Ring<MODE>::stage;
                     tma_load_2d(stg, &tmK, &s.full_k[sk], kb * BK, tile * BM, pol_stream);
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nkb; kb++, g++) {
                     const int sq = g % QST;
-                    mbar_wait(&s.empty_q[sq], ((g / QST) & 1) ^ 1);
+                    mbar_wait_lazy(&s.empty_q[sq], ((g / QST) & 1) ^ 1);
                     mbar_arrive_tx(&s.full_q[sq], 2 * QTILE);
                     bulk_load(s.q[sq], p.qsplit + (size_t)kb * (2 * BN * BK), 2 * QTILE, &s.full_q[sq], pol_keep);
                 }
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nkb; kb++, g++) {
                     const int sk = g % KST;
-                    mbar_wait(&s.staged[sk], (g / KST) & 1);
+                    mbar_wait_lazy(&s.staged[sk], (g / KST) & 1);
                     tma_store_2d(&tmKh, s.buf + sk * Ring<MODE>::stage, kb * BK, tile * BM, pol_out);
                     const bool group_end = (kb % CODE_KB) == CODE_KB - 1 || kb == nkb - 1;
                     if (group_end)
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int j = 0; j < BN; j++) acc[j] = 0.0;
             for (int c = 0; c < nchunks; c++, gc++) {
                 const int ab = gc & 1;
-                mbar_wait(&s.full_acc[ab], (gc >> 1) & 1);
+                mbar_wait_lazy(&s.full_acc[ab], (gc >> 1) & 1);
                 tc_fence_after();
                 uint32_t v[32];
 #pragma unroll

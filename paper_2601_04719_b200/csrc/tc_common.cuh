@@ -42,6 +42,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
     while (!mbar_try_wait(a, parity)) {
     }
 }
+// For roles that mostly wait (epilogue, store warp, producers): back off between
+// polls so idle warps do not burn issue slots and power under the 1 kW cap.
+__device__ __forceinline__ void mbar_wait_lazy(uint64_t *b, uint32_t parity) {
+    const uint32_t a = smem_u32(b);
+    while (!mbar_try_wait(a, parity)) __nanosleep(64);
+}
 
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int x, int y,

@@ -1,0 +1,25 @@
+"""Exercise every libkvq entry point on small ragged shapes (for compute-sanitizer)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2601_04719_b200 import kvq  # noqa: E402
+
+torch.cuda.set_device(0)
+for (T, D, nq) in [(300, 64, 7), (129, 48, 64), (77, 13, 5), (1, 4, 1), (257, 1024, 64)]:
+    K = kvq.kvq_synth_fill(T, D, seed=42, dist=1)
+    Q = kvq.kvq_synth_fill(nq, D, seed=43)
+    s = kvq.kvq_compute_scales(K)
+    q = kvq.kvq_quantize(K, s)
+    kh = kvq.kvq_dequantize(q, s)
+    q2, kh2 = kvq.kvq_quantize_dequantize(K, s)
+    m = kvq.kvq_error_metrics(K, kh, Q, s)
+    q3, kh3, out = kvq.kvq_roundtrip(K, s, Q)
+    S = kvq.kvq_attention_scores(Q, K, kh)
+    s4, q4, kh4, single = kvq.kvq_quantize_fused(K)
+    r = kvq.kvq_roundtrip_host(K.cpu().pin_memory(), Q.cpu().pin_memory())
+    torch.cuda.synchronize()
+    assert torch.equal(q, q2) and torch.equal(q, q3) and torch.equal(q, q4)
+    print(T, D, nq, "ok", m["attn_mean_abs"], single)
