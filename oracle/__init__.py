@@ -61,6 +61,13 @@ def lib():
         L.kvqo_attention_abs_sum.argtypes = [vp, i64, vp, vp, i64, i64]
         L.kvqo_theoretical_max.restype = ctypes.c_double
         L.kvqo_theoretical_max.argtypes = [vp, i64]
+        L.kvqo_e4m3_decode.restype = ctypes.c_float
+        L.kvqo_e4m3_decode.argtypes = [ctypes.c_uint8]
+        L.kvqo_e4m3_encode.restype = ctypes.c_uint8
+        L.kvqo_e4m3_encode.argtypes = [ctypes.c_float]
+        L.kvqo_scales_from_absmax_e4m3.argtypes = [vp, i64, vp]
+        L.kvqo_quantize_e4m3.argtypes = [vp, vp, i64, i64, vp]
+        L.kvqo_dequantize_e4m3.argtypes = [vp, vp, i64, i64, vp]
         _lib = L
     return _lib
 
@@ -172,6 +179,48 @@ def attention_error(Q, K, K_hat) -> float:
 def theoretical_max(scales) -> float:
     scales = _f32(scales)
     return float(lib().kvqo_theoretical_max(_p(scales), scales.shape[0]))
+
+
+# --------------------------------------------------------------------------- FP8 E4M3 variant (NEXT-1)
+def e4m3_decode(c: int) -> float:
+    return float(lib().kvqo_e4m3_decode(c))
+
+
+def e4m3_encode(v: float) -> int:
+    return int(lib().kvqo_e4m3_encode(v))
+
+
+def compute_scales_e4m3(K) -> np.ndarray:
+    """s_d = max_t |K[t,d]| / 448 (Alg. 1's max, E4M3 range; reading Q17)."""
+    K = _f32(K)
+    m = np.zeros(K.shape[1], dtype=np.float32)
+    absmax_rows(K, m)
+    s = np.empty_like(m)
+    lib().kvqo_scales_from_absmax_e4m3(_p(m), m.shape[0], _p(s))
+    return s
+
+
+def quantize_e4m3(K, scales) -> np.ndarray:
+    K, scales = _f32(K), _f32(scales)
+    T, D = K.shape
+    q = np.empty((T, D), dtype=np.uint8)
+    lib().kvqo_quantize_e4m3(_p(K), _p(scales), T, D, _p(q))
+    return q
+
+
+def dequantize_e4m3(q, scales) -> np.ndarray:
+    q = np.ascontiguousarray(q, dtype=np.uint8)
+    scales = _f32(scales)
+    T, D = q.shape
+    out = np.empty((T, D), dtype=np.float32)
+    lib().kvqo_dequantize_e4m3(_p(q), _p(scales), T, D, _p(out))
+    return out
+
+
+def roundtrip_e4m3(K):
+    s = compute_scales_e4m3(K)
+    q = quantize_e4m3(K, s)
+    return s, q, dequantize_e4m3(q, s)
 
 
 # --------------------------------------------------------------------------- whole pipeline

@@ -26,6 +26,10 @@
  *   kvqo_scores / kvqo_attention_abs_sum
  *                                    pinned: [[1]] vs [[0.9]] -> 0.1, identity,
  *                                    numpy float64 matmul, closed form sqrt(2/pi) s sqrt(D/36)
+ *   kvqo_e4m3_encode / _decode, kvqo_*_e4m3 (NEXT-1 FP8 variant)
+ *                                    pinned: hand-worked E4M3 codes incl. ties and saturation,
+ *                                    torch float8_e4m3fn on all 256 codes and exhaustively over
+ *                                    every fp32 in [2^-12, 448), numpy abs-max / 448
  *   No function is "parity unpinned".
  */
 #include <math.h>
@@ -231,4 +235,79 @@ double kvqo_theoretical_max(const float *scales, int64_t D)
         if ((double)scales[d] / 2.0 > m)
             m = (double)scales[d] / 2.0;
     return m;
+}
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-1 (paper future work "FP8"): per-channel FP8   */
+/* E4M3 variant.  Reading Q17: s_d = max_t |K[t,d]| / 448    */
+/* (448 = largest finite E4M3), code = E4M3 round-to-nearest-even of the     */
+/* fp32 IEEE quotient with saturation to +-448 (OCP "satfinite"), s_d == 0   */
+/* gives code 0 (+0), K_hat = decode(code) * s_d in fp32.                   */
+/* E4M3 (OCP FP8 "e4m3fn"): sign, 4 exponent bits (bias 7), 3 mantissa bits, */
+/* no infinities, S.1111.111 = NaN; normal (1 + M/8) 2^(E-7), subnormal      */
+/* (M/8) 2^-6.                                                               */
+/* ------------------------------------------------------------------------ */
+
+float kvqo_e4m3_decode(uint8_t c)
+{
+    int sgn = c >> 7, E = (c >> 3) & 15, M = c & 7;
+    float v;
+    if (E == 15 && M == 7)
+        return NAN;
+    if (E == 0)
+        v = ldexpf((float)M / 8.0f, -6);
+    else
+        v = ldexpf(1.0f + (float)M / 8.0f, E - 7);
+    return sgn ? -v : v;
+}
+
+uint8_t kvqo_e4m3_encode(float v)
+{
+    uint8_t sgn = signbit(v) ? 0x80 : 0x00;
+    float a = fabsf(v);
+    if (isnan(v))
+        return 0x7F;
+    if (a >= 448.0f) /* every value >= 448 rounds to 448 or beyond it: saturate */
+        return sgn | 0x7E;
+    if (a == 0.0f)
+        return sgn;
+    int e;
+    frexpf(a, &e); /* a = m 2^e, m in [0.5, 1): floor(log2 a) = e - 1 */
+    int E = e - 1;
+    if (E < -6)
+        E = -6; /* subnormals share the quantum of the 2^-6 binade */
+    float quantum = ldexpf(1.0f, E - 3);
+    float r = rintf(a / quantum); /* exact scaling by a power of two; half-even */
+    float val = r * quantum;
+    if (val == 0.0f)
+        return sgn;
+    if (val < 0x1p-6f) /* subnormal: M = val / 2^-9 in 1..7 */
+        return sgn | (uint8_t)(val / 0x1p-9f);
+    frexpf(val, &e);
+    E = e - 1;
+    int M = (int)(val / ldexpf(1.0f, E - 3)) - 8;
+    return sgn | (uint8_t)(((E + 7) << 3) | M);
+}
+
+/* scales for E4M3: s_d = max_abs / 448 (fp32 division) */
+void kvqo_scales_from_absmax_e4m3(const float *max_abs, int64_t D, float *scales)
+{
+    for (int64_t d = 0; d < D; d++)
+        scales[d] = max_abs[d] / 448.0f;
+}
+
+void kvqo_quantize_e4m3(const float *K, const float *scales, int64_t T, int64_t D, uint8_t *Kq)
+{
+    for (int64_t t = 0; t < T; t++)
+        for (int64_t d = 0; d < D; d++) {
+            float s = scales[d];
+            Kq[t * D + d] = (s == 0.0f) ? 0 : kvqo_e4m3_encode(K[t * D + d] / s);
+        }
+}
+
+void kvqo_dequantize_e4m3(const uint8_t *Kq, const float *scales, int64_t T, int64_t D, float *K_hat)
+{
+    for (int64_t t = 0; t < T; t++)
+        for (int64_t d = 0; d < D; d++)
+            K_hat[t * D + d] = kvqo_e4m3_decode(Kq[t * D + d]) * scales[d];
 }
