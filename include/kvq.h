@@ -48,6 +48,10 @@ typedef enum {
     KVQ_ERR_UNSUPPORTED = 4    /* current device is not sm_100 */
 } kvq_status;
 
+/* Code formats.  KVQ_FMT_INT8 is the paper's method; KVQ_FMT_E4M3 the FP8 variant
+ * of its future work (reading Q17). */
+typedef enum { KVQ_FMT_INT8 = 0, KVQ_FMT_E4M3 = 1 } kvq_format;
+
 /* Opaque multi-GPU communicator (wraps an ncclComm_t; NULL = single GPU). */
 typedef struct kvq_comm_s *kvq_comm_t;
 
@@ -90,6 +94,11 @@ kvq_status kvq_comm_destroy(kvq_comm_t comm);
 kvq_status kvq_compute_scales(const float *K, int64_t T, int64_t D, float *scales,
                               kvq_comm_t comm, void *stream);
 
+/* Same as kvq_compute_scales with the divisor of `fmt`: 127 (KVQ_FMT_INT8) or
+ * 448 (KVQ_FMT_E4M3, the largest finite E4M3 value). */
+kvq_status kvq_compute_scales_fmt(const float *K, int64_t T, int64_t D, float *scales, int fmt,
+                                  kvq_comm_t comm, void *stream);
+
 /* a3: Eq. 7 / Listing 3:
  *   Kq[t,d] = clamp(round_half_even(fl32(K[t,d] / scales[d])), -127, 127),
  *   and 0 where scales[d] == 0                   (readings Q1, Q2, Q4, Q5)
@@ -102,6 +111,16 @@ kvq_status kvq_quantize(const float *K, const float *scales, int64_t T, int64_t 
  * Kq: [T][D] int8 in; scales: [D] in; K_hat: [T][D] float32 out (may not alias Kq). */
 kvq_status kvq_dequantize(const int8_t *Kq, const float *scales, int64_t T, int64_t D,
                           float *K_hat, void *stream);
+
+/* FP8 E4M3 variant of a3 (+a4) (P:570 future work; reading Q17):
+ *   Kq8[t,d] = E4M3_RN_satfinite(fl32(K[t,d] / scales[d]))  (0x00 where scales[d] == 0)
+ *   K_hat[t,d] = decode(Kq8[t,d]) * scales[d]               (if K_hat != NULL)
+ * Codes are OCP E4M3 ("e4m3fn") bytes; scales from kvq_compute_scales_fmt(KVQ_FMT_E4M3).
+ * Bit-identical to the oracle's kvqo_quantize_e4m3 / kvqo_dequantize_e4m3. */
+kvq_status kvq_quantize_e4m3(const float *K, const float *scales, int64_t T, int64_t D,
+                             uint8_t *Kq8, float *K_hat, void *stream);
+kvq_status kvq_dequantize_e4m3(const uint8_t *Kq8, const float *scales, int64_t T, int64_t D,
+                               float *K_hat, void *stream);
 
 /* a3+a4 fused in one pass over K (9 B/elem instead of 10): writes both Kq and
  * K_hat, bit-identical to kvq_quantize followed by kvq_dequantize. */

@@ -39,6 +39,9 @@ SIGNATURES = {
     "kvq_comm_init": (_int, [ctypes.POINTER(_vp), _vp, _int, _int]),
     "kvq_comm_destroy": (_int, [_vp]),
     "kvq_compute_scales": (_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
+    "kvq_compute_scales_fmt": (_int, [_vp, _i64, _i64, _vp, _int, _vp, _vp]),
+    "kvq_quantize_e4m3": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "kvq_dequantize_e4m3": (_int, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "kvq_quantize": (_int, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "kvq_dequantize": (_int, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "kvq_quantize_dequantize": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp]),

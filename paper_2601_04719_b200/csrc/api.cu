@@ -128,10 +128,11 @@ extern "C" const char *kvq_last_error(void) { return g_last_error.c_str(); }
 extern "C" kvq_status kvq_device_check(void) { return device_ok(); }
 
 // ------------------------------------------------------------------------------ a1 + a2 (+ a7)
-extern "C" kvq_status kvq_compute_scales(const float *K, int64_t T, int64_t D, float *scales, kvq_comm_t comm,
-                                         void *stream) {
+extern "C" kvq_status kvq_compute_scales_fmt(const float *K, int64_t T, int64_t D, float *scales, int fmt,
+                                             kvq_comm_t comm, void *stream) {
     KVQ_REQUIRE(K && scales, "kvq_compute_scales: NULL pointer");
     KVQ_REQUIRE(!bad_dims(T, D), "kvq_compute_scales: need T >= 1, D >= 1, T*D <= 2^62");
+    KVQ_REQUIRE(fmt == KVQ_FMT_INT8 || fmt == KVQ_FMT_E4M3, "kvq_compute_scales: unknown format");
     KVQ_REQUIRE(!overlap(K, (size_t)(T * D) * 4, scales, (size_t)D * 4), "kvq_compute_scales: scales aliases K");
     KVQ_TRY(device_ok());
     cudaStream_t s = (cudaStream_t)stream;
@@ -139,7 +140,39 @@ extern "C" kvq_status kvq_compute_scales(const float *K, int64_t T, int64_t D, f
     KVQ_TRY(cuda_check(cudaMemsetAsync(bits, 0, (size_t)D * 4, s), "memset scales"));
     KVQ_TRY(launch_colmax(K, T, D, bits, s));
     if (comm) KVQ_TRY(comm_allreduce_max_u32(comm, bits, (size_t)D, s));
-    return launch_finalize(bits, D, s);
+    return launch_finalize(bits, D, s, fmt == KVQ_FMT_E4M3 ? 448.0f : 127.0f);
+}
+
+extern "C" kvq_status kvq_compute_scales(const float *K, int64_t T, int64_t D, float *scales, kvq_comm_t comm,
+                                         void *stream) {
+    return kvq_compute_scales_fmt(K, T, D, scales, KVQ_FMT_INT8, comm, stream);
+}
+
+// ------------------------------------------------------------------------------ FP8 E4M3 variant (NEXT-1)
+extern "C" kvq_status kvq_quantize_e4m3(const float *K, const float *scales, int64_t T, int64_t D, uint8_t *Kq8,
+                                        float *K_hat, void *stream) {
+    KVQ_REQUIRE(K && scales && Kq8, "kvq_quantize_e4m3: NULL pointer");
+    KVQ_REQUIRE(!bad_dims(T, D), "kvq_quantize_e4m3: need T >= 1, D >= 1, T*D <= 2^62");
+    const size_t n = (size_t)(T * D);
+    KVQ_REQUIRE(!overlap(K, n * 4, Kq8, n) && !overlap(scales, (size_t)D * 4, Kq8, n),
+                "kvq_quantize_e4m3: Kq8 aliases an input");
+    if (K_hat)
+        KVQ_REQUIRE(!overlap(K_hat, n * 4, K, n * 4) && !overlap(K_hat, n * 4, Kq8, n) &&
+                        !overlap(K_hat, n * 4, scales, (size_t)D * 4),
+                    "kvq_quantize_e4m3: K_hat aliases an input");
+    KVQ_TRY(device_ok());
+    return launch_quantize_e4m3(K, scales, T, D, Kq8, K_hat, (cudaStream_t)stream);
+}
+
+extern "C" kvq_status kvq_dequantize_e4m3(const uint8_t *Kq8, const float *scales, int64_t T, int64_t D,
+                                          float *K_hat, void *stream) {
+    KVQ_REQUIRE(Kq8 && scales && K_hat, "kvq_dequantize_e4m3: NULL pointer");
+    KVQ_REQUIRE(!bad_dims(T, D), "kvq_dequantize_e4m3: need T >= 1, D >= 1, T*D <= 2^62");
+    const size_t n = (size_t)(T * D);
+    KVQ_REQUIRE(!overlap(K_hat, n * 4, Kq8, n) && !overlap(K_hat, n * 4, scales, (size_t)D * 4),
+                "kvq_dequantize_e4m3: K_hat aliases an input");
+    KVQ_TRY(device_ok());
+    return launch_dequantize_e4m3(Kq8, scales, T, D, K_hat, (cudaStream_t)stream);
 }
 
 // ------------------------------------------------------------------------------ a3, a4

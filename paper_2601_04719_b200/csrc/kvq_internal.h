@@ -37,7 +37,12 @@ StreamPlan plan_stream(int64_t rows, int64_t cols, int threads_per_sm);
 
 // ---- quantization kernels (quant_kernels.cu)
 kvq_status launch_colmax(const float *K, int64_t T, int64_t D, uint32_t *mbits, cudaStream_t s);
-kvq_status launch_finalize(uint32_t *mbits_to_scales, int64_t D, cudaStream_t s);
+kvq_status launch_finalize(uint32_t *mbits_to_scales, int64_t D, cudaStream_t s, float divisor = 127.0f);
+// ---- FP8 E4M3 variant (fp8_kernels.cu)
+kvq_status launch_quantize_e4m3(const float *K, const float *scales, int64_t T, int64_t D, uint8_t *Kq,
+                                float *K_hat /* nullable */, cudaStream_t s);
+kvq_status launch_dequantize_e4m3(const uint8_t *Kq, const float *scales, int64_t T, int64_t D, float *K_hat,
+                                  cudaStream_t s);
 kvq_status launch_quantize(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
                            float *K_hat /* nullable: fused a3+a4 */, cudaStream_t s);
 kvq_status launch_dequantize(const int8_t *Kq, const float *scales, int64_t T, int64_t D, float *K_hat,

@@ -103,10 +103,11 @@ __global__ void __launch_bounds__(kThreads) colmax_scalar_kernel(const float *__
 
 // ============================================================================ a2: finalize
 // s_d = fl32(m_d / 127.0f), IEEE division (reading Q3); in place.
-__global__ void finalize_kernel(uint32_t *buf, int64_t D) {
+// (divisor 448 for the E4M3 variant, reading Q17)
+__global__ void finalize_kernel(uint32_t *buf, int64_t D, float divisor) {
     for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < D; d += (int64_t)gridDim.x * blockDim.x) {
         float m = __uint_as_float(buf[d]);
-        reinterpret_cast<float *>(buf)[d] = __fdiv_rn(m, 127.0f);
+        reinterpret_cast<float *>(buf)[d] = __fdiv_rn(m, divisor);
     }
 }
 
@@ -402,9 +403,9 @@ kvq_status launch_colmax(const float *K, int64_t T, int64_t D, uint32_t *mbits, 
     return check_launch("colmax");
 }
 
-kvq_status launch_finalize(uint32_t *buf, int64_t D, cudaStream_t s) {
+kvq_status launch_finalize(uint32_t *buf, int64_t D, cudaStream_t s, float divisor) {
     unsigned blocks = (unsigned)std::min<int64_t>((D + 255) / 256, 1024);
-    finalize_kernel<<<blocks, 256, 0, s>>>(buf, D);
+    finalize_kernel<<<blocks, 256, 0, s>>>(buf, D, divisor);
     return check_launch("finalize");
 }
 

@@ -18,7 +18,8 @@ __all__ = [
     "kvq_error_metrics", "kvq_error_metrics_async", "kvq_error_metrics_workspace_size", "kvq_attention_scores",
     "kvq_roundtrip_host", "kvq_roundtrip_host_workspace_size", "kvq_synth_fill", "kvq_device_check",
     "kvq_comm_unique_id", "METRICS_BYTES", "metrics_from_device", "kvq_roundtrip", "kvq_roundtrip_workspace_size",
-    "kvq_quantize_fused", "kvq_roundtrip_host_async", "metrics_from_host",
+    "kvq_quantize_fused", "kvq_roundtrip_host_async", "metrics_from_host", "kvq_compute_scales_fmt",
+    "kvq_quantize_e4m3", "kvq_dequantize_e4m3", "FMT_INT8", "FMT_E4M3",
 ]
 
 load()  # fail loudly at import if libkvq.so cannot be loaded or built
@@ -101,6 +102,45 @@ def kvq_compute_scales(K: torch.Tensor, scales: Optional[torch.Tensor] = None, c
     check(load().kvq_compute_scales(_ptr(K), T, D, _ptr(scales), _comm_handle(comm), _stream(stream)),
           "kvq_compute_scales")
     return scales
+
+
+FMT_INT8, FMT_E4M3 = 0, 1
+
+
+def kvq_compute_scales_fmt(K: torch.Tensor, fmt: int, scales: Optional[torch.Tensor] = None,
+                           comm: Optional[Comm] = None, stream=None) -> torch.Tensor:
+    T, D = _mat(K, torch.float32, "K")
+    if scales is None:
+        scales = torch.empty(D, dtype=torch.float32, device=K.device)
+    _vec(scales, D, "scales")
+    check(load().kvq_compute_scales_fmt(_ptr(K), T, D, _ptr(scales), fmt, _comm_handle(comm), _stream(stream)),
+          "kvq_compute_scales_fmt")
+    return scales
+
+
+def kvq_quantize_e4m3(K: torch.Tensor, scales: torch.Tensor, Kq8: Optional[torch.Tensor] = None,
+                      K_hat: Optional[torch.Tensor] = None, want_khat: bool = False, stream=None):
+    """FP8 E4M3 codes (uint8, OCP e4m3fn bytes); also K_hat when given or want_khat."""
+    T, D = _mat(K, torch.float32, "K")
+    _vec(scales, D, "scales")
+    if Kq8 is None:
+        Kq8 = torch.empty((T, D), dtype=torch.uint8, device=K.device)
+    if K_hat is None and want_khat:
+        K_hat = torch.empty((T, D), dtype=torch.float32, device=K.device)
+    check(load().kvq_quantize_e4m3(_ptr(K), _ptr(scales), T, D, _ptr(Kq8), _ptr(K_hat), _stream(stream)),
+          "kvq_quantize_e4m3")
+    return (Kq8, K_hat) if K_hat is not None else Kq8
+
+
+def kvq_dequantize_e4m3(Kq8: torch.Tensor, scales: torch.Tensor, K_hat: Optional[torch.Tensor] = None,
+                        stream=None) -> torch.Tensor:
+    T, D = _mat(Kq8, torch.uint8, "Kq8")
+    _vec(scales, D, "scales")
+    if K_hat is None:
+        K_hat = torch.empty((T, D), dtype=torch.float32, device=Kq8.device)
+    check(load().kvq_dequantize_e4m3(_ptr(Kq8), _ptr(scales), T, D, _ptr(K_hat), _stream(stream)),
+          "kvq_dequantize_e4m3")
+    return K_hat
 
 
 def kvq_quantize(K: torch.Tensor, scales: torch.Tensor, Kq: Optional[torch.Tensor] = None,
