@@ -35,7 +35,7 @@ CONFIGS = {  # BASELINE.json configs
 }
 METRIC = "quantize+dequantize elements/s and achieved HBM GB/s vs B200 peak at 1/2/4/8 GPUs"
 # Algorithmic bytes per element of each pass: what the method itself must move.
-BYTES = {"scales": 4, "quantize": 5, "dequantize": 5, "metrics": 8, "roundtrip": 9}
+BYTES = {"scales": 4, "quantize": 5, "dequantize": 5, "metrics": 8, "roundtrip": 9, "quantize_dequantize_e4m3": 9}
 
 
 def measured_traffic(kernel: str):
@@ -221,9 +221,28 @@ def run_kvq(args, cfg, rank, world, local_rank):
         if ev is not None:
             ev[2].record(stream)
 
-    step = step_fused if args.pipeline == "fused" else step_separate
-    pass_names = ["scales", "roundtrip"] if args.pipeline == "fused" else ["scales", "quantize", "dequantize",
-                                                                            "metrics"]
+    Kq8 = torch.empty((rows, D), dtype=torch.uint8, device=dev) if args.format == "e4m3" else None
+
+    def step_e4m3(ev=None):
+        """FP8 E4M3 variant (NEXT-1): scales (/448), fused quantize+dequantize, fidelity checks."""
+        if ev is not None:
+            ev[0].record(stream)
+        kvq.kvq_compute_scales_fmt(K, kvq.FMT_E4M3, scales, comm=comm, stream=stream)
+        if ev is not None:
+            ev[1].record(stream)
+        kvq.kvq_quantize_e4m3(K, scales, Kq8, Kh, stream=stream)
+        if ev is not None:
+            ev[2].record(stream)
+        kvq.kvq_error_metrics_async(K, Kh, Q, scales, out_dev=mout, workspace=ws, comm=comm, stream=stream)
+        if ev is not None:
+            ev[3].record(stream)
+
+    if args.format == "e4m3":
+        step, pass_names = step_e4m3, ["scales", "quantize_dequantize_e4m3", "metrics"]
+    elif args.pipeline == "fused":
+        step, pass_names = step_fused, ["scales", "roundtrip"]
+    else:
+        step, pass_names = step_separate, ["scales", "quantize", "dequantize", "metrics"]
 
     for _ in range(args.warmup):
         step()
@@ -266,7 +285,7 @@ def run_kvq(args, cfg, rank, world, local_rank):
     # streams / workspaces alternate so step i's device->host copy overlaps step i+1's
     # host->device copy (kvq_roundtrip_host_async uses separate H2D and D2H copy engines).
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.format == "int8":
         del Kq, Kh, ws
         torch.cuda.empty_cache()
         K_host = K.cpu().pin_memory()
@@ -337,17 +356,19 @@ def run_kvq(args, cfg, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (splitmix64 lattice uniform [-1,1), SURVEY §8(d))",
         "config": {"workload": f"{cfg['name']}: {cfg['desc']}", "T": T, "D": D, "nq": nq,
-                   "step": ("kvq_compute_scales(a1,a2,+a7 allreduce MAX) -> kvq_roundtrip(a3 quantize, a4 dequantize,"
-                            " a5 L2/max, a6 attention error; one HBM pass)") if args.pipeline == "fused" else
-                           "kvq_compute_scales -> kvq_quantize -> kvq_dequantize -> kvq_error_metrics_async",
-                   "pipeline": args.pipeline,
+                   "step": ("kvq_compute_scales_fmt(E4M3) -> kvq_quantize_e4m3(+K_hat) -> kvq_error_metrics_async"
+                            if args.format == "e4m3" else
+                            ("kvq_compute_scales(a1,a2,+a7 allreduce MAX) -> kvq_roundtrip(a3 quantize, a4 dequantize,"
+                             " a5 L2/max, a6 attention error; one HBM pass)") if args.pipeline == "fused" else
+                            "kvq_compute_scales -> kvq_quantize -> kvq_dequantize -> kvq_error_metrics_async"),
+                   "pipeline": args.pipeline, "format": args.format,
                    "l2_flush": "none needed: inputs larger than L2 (K alone is %.2f GB > 126 MB)" % (4 * T * D / 1e9)
                    if 4 * T * D > 2 * 126e6 else "inputs L2-resident (warm)",
                    "parallelism": f"token-shard x{world}", "comm": "nccl (libkvq kvq_comm_t)" if comm else None},
         "hbm": {"GBps": algo_bytes / (ms * 1e-3) / 1e9 / world, "algo_bytes_per_elem": algo_per_elem,
                 "frac_of_peak_per_gpu": algo_bytes / (ms * 1e-3) / 1e9 / world / pk["hbm_gbs"]},
         "passes": pass_report, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": (7 if args.pipeline == "fused" else 8) * args.steps, "clocks": clk.summary(wall0, wall1),
+        "gpu_launches": (7 if args.format == "e4m3" else 7 if args.pipeline == "fused" else 8) * args.steps, "clocks": clk.summary(wall0, wall1),
         "fidelity": {k: metrics[k] for k in ("l2", "max_abs", "attn_mean_abs", "theoretical_max")},
     }
     print(json.dumps(line), flush=True)
@@ -361,6 +382,8 @@ def main():
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="kvq", choices=["kvq", "reference"])
     ap.add_argument("--pipeline", default="fused", choices=["fused", "separate"])
+    ap.add_argument("--format", default="int8", choices=["int8", "e4m3"],
+                    help="int8 = the paper's method (headline); e4m3 = the FP8 variant (NEXT-1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=6)
