@@ -191,6 +191,22 @@ kvq_status kvq_attention_scores(const float *Q, int64_t nq, const float *K, cons
                                 int64_t T, int64_t D, float *S, void *workspace, size_t workspace_bytes,
                                 void *stream);
 
+/* NEXT-2: raw attention scores computed directly from the
+ * compressed cache, without materialising K_hat ("dequantize them back ...
+ * when needed for attention"; P:24 raw dot products, reading Q10):
+ *   S[i][t] = sum_d Q[i][d] * (Kq[t][d] * scales[d])
+ * Q: [nq][D] fp32, Kq: [T][D] int8 codes, scales: [D], S: [nq][T] fp32 out.
+ * With a workspace of kvq_scores_from_codes_workspace_size(D, nq) bytes,
+ * 1 <= nq <= 64, D % 16 == 0 and 16-byte aligned Kq this runs on the tcgen05
+ * tensor cores (kind::f16: codes exact in bf16, Q*s split into bf16 hi+lo,
+ * fp32 TMEM accumulation carried in fp64 per 256 columns) reading 1 byte per
+ * key element; otherwise a CUDA-core kernel (fp64 sums).  Within 1e-5 of
+ * sum_d Q[i][d]*K_hat[t][d] relative to sum_d |Q[i][d]*K_hat[t][d]|. */
+size_t kvq_scores_from_codes_workspace_size(int64_t D, int64_t nq);
+kvq_status kvq_scores_from_codes(const float *Q, int64_t nq, const int8_t *Kq, const float *scales,
+                                 int64_t T, int64_t D, float *S, void *workspace, size_t workspace_bytes,
+                                 void *stream);
+
 /* ---------------------------------------------------------------- host-buffer pipeline */
 /* The whole path from HOST memory (the end-to-end call a user makes):
  * H2D of K (row blocks, overlapped with the column-max kernel), scales,

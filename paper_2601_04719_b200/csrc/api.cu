@@ -333,6 +333,25 @@ extern "C" kvq_status kvq_attention_scores(const float *Q, int64_t nq, const flo
     return launch_attention_scores(Q, nq, K, K_hat, T, D, S, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
+// ------------------------------------------------------------------------------ NEXT-2: scores from codes
+extern "C" size_t kvq_scores_from_codes_workspace_size(int64_t D, int64_t nq) {
+    if (D < 1 || nq < 1) return 0;
+    return scores_codes_workspace_size(D);
+}
+
+extern "C" kvq_status kvq_scores_from_codes(const float *Q, int64_t nq, const int8_t *Kq, const float *scales,
+                                            int64_t T, int64_t D, float *S, void *workspace, size_t workspace_bytes,
+                                            void *stream) {
+    KVQ_REQUIRE(Q && Kq && scales && S, "kvq_scores_from_codes: NULL pointer");
+    KVQ_REQUIRE(!bad_dims(T, D) && nq >= 1 && nq <= (int64_t(1) << 62) / T && nq <= (int64_t(1) << 62) / D,
+                "kvq_scores_from_codes: bad sizes");
+    KVQ_REQUIRE(!overlap(S, (size_t)(nq * T) * 4, Kq, (size_t)(T * D)) &&
+                    !overlap(S, (size_t)(nq * T) * 4, Q, (size_t)(nq * D) * 4),
+                "kvq_scores_from_codes: S aliases an input");
+    KVQ_TRY(device_ok());
+    return launch_scores_codes(Q, nq, Kq, scales, T, D, S, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
 // ------------------------------------------------------------------------------ host-buffer pipeline
 namespace {
 struct HostLayout {

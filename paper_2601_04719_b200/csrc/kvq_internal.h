@@ -87,6 +87,11 @@ size_t attention_scores_workspace_size(int64_t D, int64_t nq);
 kvq_status launch_attention_scores(const float *Q, int64_t nq, const float *K, const float *K_hat, int64_t T,
                                    int64_t D, float *S, void *ws, size_t ws_bytes, cudaStream_t s);
 
+// ---- scores from codes (scores_codes.cu, NEXT-2)
+size_t scores_codes_workspace_size(int64_t D);
+kvq_status launch_scores_codes(const float *Q, int64_t nq, const int8_t *Kq, const float *scales, int64_t T,
+                               int64_t D, float *S, void *ws, size_t ws_bytes, cudaStream_t s);
+
 // ---- comm (comm.cpp)
 kvq_status comm_allreduce_max_u32(kvq_comm_t comm, uint32_t *buf, size_t count, cudaStream_t s);
 kvq_status comm_allreduce_sum_f64(kvq_comm_t comm, double *buf, size_t count, cudaStream_t s);

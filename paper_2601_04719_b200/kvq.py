@@ -19,7 +19,7 @@ __all__ = [
     "kvq_roundtrip_host", "kvq_roundtrip_host_workspace_size", "kvq_synth_fill", "kvq_device_check",
     "kvq_comm_unique_id", "METRICS_BYTES", "metrics_from_device", "kvq_roundtrip", "kvq_roundtrip_workspace_size",
     "kvq_quantize_fused", "kvq_roundtrip_host_async", "metrics_from_host", "kvq_compute_scales_fmt",
-    "kvq_quantize_e4m3", "kvq_dequantize_e4m3", "FMT_INT8", "FMT_E4M3",
+    "kvq_quantize_e4m3", "kvq_dequantize_e4m3", "FMT_INT8", "FMT_E4M3", "kvq_scores_from_codes",
 ]
 
 load()  # fail loudly at import if libkvq.so cannot be loaded or built
@@ -298,6 +298,24 @@ def kvq_attention_scores(Q: torch.Tensor, K: torch.Tensor, K_hat: Optional[torch
     nbytes = 0 if workspace is None else workspace.numel()
     check(load().kvq_attention_scores(_ptr(Q), nq, _ptr(K), _ptr(K_hat), T, D, _ptr(S), _ptr(workspace), nbytes,
                                       _stream(stream)), "kvq_attention_scores")
+    return S
+
+
+def kvq_scores_from_codes(Q: torch.Tensor, Kq: torch.Tensor, scales: torch.Tensor,
+                          S: Optional[torch.Tensor] = None, workspace="auto", stream=None) -> torch.Tensor:
+    """S[i][t] = sum_d Q[i][d] * Kq[t][d] * scales[d] from the int8 codes (tensor cores when eligible)."""
+    nq, D = _mat(Q, torch.float32, "Q")
+    T, D2 = _mat(Kq, torch.int8, "Kq")
+    assert D == D2
+    _vec(scales, D, "scales")
+    if S is None:
+        S = torch.empty((nq, T), dtype=torch.float32, device=Kq.device)
+    if isinstance(workspace, str):
+        workspace = torch.empty(int(load().kvq_scores_from_codes_workspace_size(D, nq)), dtype=torch.uint8,
+                                device=Kq.device)
+    nbytes = 0 if workspace is None else workspace.numel()
+    check(load().kvq_scores_from_codes(_ptr(Q), nq, _ptr(Kq), _ptr(scales), T, D, _ptr(S), _ptr(workspace), nbytes,
+                                       _stream(stream)), "kvq_scores_from_codes")
     return S
 
 
