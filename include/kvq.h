@@ -197,11 +197,17 @@ kvq_status kvq_attention_scores(const float *Q, int64_t nq, const float *K, cons
  *   S[i][t] = sum_d Q[i][d] * (Kq[t][d] * scales[d])
  * Q: [nq][D] fp32, Kq: [T][D] int8 codes, scales: [D], S: [nq][T] fp32 out.
  * With a workspace of kvq_scores_from_codes_workspace_size(D, nq) bytes,
- * 1 <= nq <= 64, D % 16 == 0 and 16-byte aligned Kq this runs on the tcgen05
- * tensor cores (kind::f16: codes exact in bf16, Q*s split into bf16 hi+lo,
- * fp32 TMEM accumulation carried in fp64 per 256 columns) reading 1 byte per
- * key element; otherwise a CUDA-core kernel (fp64 sums).  Within 1e-5 of
- * sum_d Q[i][d]*K_hat[t][d] relative to sum_d |Q[i][d]*K_hat[t][d]|. */
+ * 1 <= nq <= 64, D % 16 == 0, D <= 264208 and 16-byte aligned Kq this runs on
+ * the tcgen05 INTEGER tensor cores (kind::i8, CTA pairs): the codes are the A
+ * operand as stored; W = fl32(Q*s) is written as 4 signed base-2^7 digits per
+ * query row under a per-row exponent (truncation |e| < 2^-27 max_d |W[i][d]|),
+ * s8 x s8 products accumulate EXACTLY in s32 and are recombined in fp64, reading
+ * 1 byte per key element.  Rows of Q with a non-finite W take an fp64
+ * per-element path (inf/nan propagate as in the definition).  Otherwise a
+ * CUDA-core kernel (fp64 sums).  Within 1e-5 of sum_d Q[i][d]*K_hat[t][d]
+ * relative to sum_d |Q[i][d]*K_hat[t][d]|; exact (before the final fp32
+ * rounding) when every W[i][d] is a multiple of 2^(E_i - 28).  Enqueues 3
+ * kernels on `stream`; the workspace must not be shared by concurrent calls. */
 size_t kvq_scores_from_codes_workspace_size(int64_t D, int64_t nq);
 kvq_status kvq_scores_from_codes(const float *Q, int64_t nq, const int8_t *Kq, const float *scales,
                                  int64_t T, int64_t D, float *S, void *workspace, size_t workspace_bytes,

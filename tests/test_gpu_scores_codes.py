@@ -52,3 +52,64 @@ def test_scores_from_codes_match_dequantized_scores(kvq, orc):
     S2 = kvq.kvq_attention_scores(Qd, kh)
     cond = (Qd.double().abs() @ kh.double().abs().T)
     assert float(((S1.double() - S2.double()).abs() / cond).max()) <= 2 * REL
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("T,D,nq", [(300, 1024, 64), (513, 4096, 7)])
+def test_scores_from_codes_exact_on_representable_w(kvq, orc, T, D, nq):
+    """Power-of-two scales and small-integer Q make W = Q*s exact in 4 base-2^7
+    digits and every oracle product/sum exact in fp64, so the int8 tensor-core
+    path (exact s32 accumulation, exact fp64 recombination) must agree BIT FOR
+    BIT with the oracle's fp64 Q . K_hat^T rounded to fp32."""
+    rng = np.random.default_rng(T + D)
+    q = rng.integers(-127, 128, (T, D)).astype(np.int8)
+    s = (2.0 ** rng.integers(-12, -4, D)).astype(np.float32)
+    Q = rng.integers(-2 ** 12, 2 ** 12, (nq, D)).astype(np.float32)
+    Kh = orc.dequantize(q, s)
+    S = kvq.kvq_scores_from_codes(dev(Q), dev(q), dev(s))
+    torch.cuda.synchronize()
+    ref = orc.scores(Q, Kh).astype(np.float32)
+    assert np.array_equal(S.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.timeout(300)
+def test_scores_from_codes_outlier_channels(kvq, orc):
+    """Outlier channels (scales spanning 2^10) and mixed-magnitude queries: the
+    digit truncation error |e| < 2^-27 max|W| stays far inside the 1e-5 bound."""
+    rng = np.random.default_rng(5)
+    T, D, nq = 1024, 2048, 64
+    K = orc.fill(T, D, 9, 1)
+    K[:, rng.choice(D, 16, replace=False)] *= 1000.0
+    s, q, Kh = orc.roundtrip(K)
+    Q = (orc.fill(nq, D, 44) * (2.0 ** rng.integers(-8, 8, (nq, 1)))).astype(np.float32)
+    S = kvq.kvq_scores_from_codes(dev(Q), dev(q), dev(s))
+    torch.cuda.synchronize()
+    ref = orc.scores(Q, Kh)
+    cond = np.abs(Q.astype(np.float64)) @ np.abs(Kh.astype(np.float64)).T
+    assert float((np.abs(S.cpu().numpy() - ref) / cond).max()) <= REL
+
+
+@pytest.mark.timeout(300)
+def test_scores_from_codes_nonfinite_query_rows(kvq, orc):
+    """Rows of Q holding inf/nan leave the digit path (exact fp64 per element):
+    inf/nan propagate exactly as in the definition; other rows are unaffected."""
+    T, D, nq = 300, 256, 6
+    K = orc.fill(T, D, 3, 0)
+    s, q, Kh = orc.roundtrip(K)
+    Q = orc.fill(nq, D, 45)
+    Q[1, 7] = np.inf
+    Q[3, 0] = np.nan
+    Q[4, 9] = -np.inf
+    S = kvq.kvq_scores_from_codes(dev(Q), dev(q), dev(s))
+    torch.cuda.synchronize()
+    S = S.cpu().numpy()
+    with np.errstate(invalid="ignore"):
+        ref = (Q.astype(np.float64) * s.astype(np.float64)) @ q.astype(np.float64).T
+    for i in (1, 3, 4):
+        assert np.array_equal(np.isnan(S[i]), np.isnan(ref[i]))
+        fin = ~np.isnan(ref[i])
+        assert np.array_equal(S[i][fin], ref[i][fin].astype(np.float32))
+    good = [0, 2, 5]
+    ref_ok = orc.scores(Q[good], Kh)
+    cond = np.abs(Q[good].astype(np.float64)) @ np.abs(Kh.astype(np.float64)).T
+    assert float((np.abs(S[good] - ref_ok) / cond).max()) <= REL
