@@ -35,7 +35,8 @@ CONFIGS = {  # BASELINE.json configs
 }
 METRIC = "quantize+dequantize elements/s and achieved HBM GB/s vs B200 peak at 1/2/4/8 GPUs"
 # Algorithmic bytes per element of each pass: what the method itself must move.
-BYTES = {"scales": 4, "quantize": 5, "dequantize": 5, "metrics": 8, "roundtrip": 9, "quantize_dequantize_e4m3": 9}
+BYTES = {"scales": 4, "quantize": 5, "dequantize": 5, "metrics": 8, "roundtrip": 9, "quantize_dequantize_e4m3": 9,
+         "quantize_dequantize_int4": 8.5, "quantize_dequantize_int2": 8.25}
 
 
 def measured_traffic(kernel: str):
@@ -237,8 +238,28 @@ def run_kvq(args, cfg, rank, world, local_rank):
         if ev is not None:
             ev[3].record(stream)
 
+    bits = {"int4": 4, "int2": 2}.get(args.format)
+    Kp = (torch.empty((rows, kvq.kvq_packed_row_bytes(D, bits)), dtype=torch.uint8, device=dev)
+          if bits else None)
+
+    def step_lowbit(ev=None):
+        """INT4 / INT2 packed variant (NEXT-3): scales (/7 or /1), fused quantize+dequantize, fidelity checks."""
+        if ev is not None:
+            ev[0].record(stream)
+        kvq.kvq_compute_scales_fmt(K, kvq.FMT_INT4 if bits == 4 else kvq.FMT_INT2, scales, comm=comm, stream=stream)
+        if ev is not None:
+            ev[1].record(stream)
+        kvq.kvq_quantize_packed(K, scales, bits, Kp, Kh, stream=stream)
+        if ev is not None:
+            ev[2].record(stream)
+        kvq.kvq_error_metrics_async(K, Kh, Q, scales, out_dev=mout, workspace=ws, comm=comm, stream=stream)
+        if ev is not None:
+            ev[3].record(stream)
+
     if args.format == "e4m3":
         step, pass_names = step_e4m3, ["scales", "quantize_dequantize_e4m3", "metrics"]
+    elif bits:
+        step, pass_names = step_lowbit, ["scales", f"quantize_dequantize_{args.format}", "metrics"]
     elif args.pipeline == "fused":
         step, pass_names = step_fused, ["scales", "roundtrip"]
     else:
@@ -358,6 +379,8 @@ def run_kvq(args, cfg, rank, world, local_rank):
         "config": {"workload": f"{cfg['name']}: {cfg['desc']}", "T": T, "D": D, "nq": nq,
                    "step": ("kvq_compute_scales_fmt(E4M3) -> kvq_quantize_e4m3(+K_hat) -> kvq_error_metrics_async"
                             if args.format == "e4m3" else
+                            f"kvq_compute_scales_fmt({args.format.upper()}) -> kvq_quantize_packed(bits={bits}, +K_hat)"
+                            " -> kvq_error_metrics_async" if bits else
                             ("kvq_compute_scales(a1,a2,+a7 allreduce MAX) -> kvq_roundtrip(a3 quantize, a4 dequantize,"
                              " a5 L2/max, a6 attention error; one HBM pass)") if args.pipeline == "fused" else
                             "kvq_compute_scales -> kvq_quantize -> kvq_dequantize -> kvq_error_metrics_async"),
@@ -368,7 +391,7 @@ def run_kvq(args, cfg, rank, world, local_rank):
         "hbm": {"GBps": algo_bytes / (ms * 1e-3) / 1e9 / world, "algo_bytes_per_elem": algo_per_elem,
                 "frac_of_peak_per_gpu": algo_bytes / (ms * 1e-3) / 1e9 / world / pk["hbm_gbs"]},
         "passes": pass_report, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": (7 if args.format == "e4m3" else 7 if args.pipeline == "fused" else 8) * args.steps, "clocks": clk.summary(wall0, wall1),
+        "gpu_launches": (7 if args.format != "int8" else 7 if args.pipeline == "fused" else 8) * args.steps, "clocks": clk.summary(wall0, wall1),
         "fidelity": {k: metrics[k] for k in ("l2", "max_abs", "attn_mean_abs", "theoretical_max")},
     }
     print(json.dumps(line), flush=True)
@@ -382,8 +405,9 @@ def main():
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="kvq", choices=["kvq", "reference"])
     ap.add_argument("--pipeline", default="fused", choices=["fused", "separate"])
-    ap.add_argument("--format", default="int8", choices=["int8", "e4m3"],
-                    help="int8 = the paper's method (headline); e4m3 = the FP8 variant (NEXT-1)")
+    ap.add_argument("--format", default="int8", choices=["int8", "e4m3", "int4", "int2"],
+                    help="int8 = the paper's method (headline); e4m3 = the FP8 variant (NEXT-1); "
+                         "int4 / int2 = the packed low-bit variants (NEXT-3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=6)

@@ -49,8 +49,9 @@ typedef enum {
 } kvq_status;
 
 /* Code formats.  KVQ_FMT_INT8 is the paper's method; KVQ_FMT_E4M3 the FP8 variant
- * of its future work (reading Q17). */
-typedef enum { KVQ_FMT_INT8 = 0, KVQ_FMT_E4M3 = 1 } kvq_format;
+ * of its future work (reading Q17); KVQ_FMT_INT4 /
+ * KVQ_FMT_INT2 the packed low-bit variants (NEXT-3; reading Q19). */
+typedef enum { KVQ_FMT_INT8 = 0, KVQ_FMT_E4M3 = 1, KVQ_FMT_INT4 = 2, KVQ_FMT_INT2 = 3 } kvq_format;
 
 /* Opaque multi-GPU communicator (wraps an ncclComm_t; NULL = single GPU). */
 typedef struct kvq_comm_s *kvq_comm_t;
@@ -94,8 +95,9 @@ kvq_status kvq_comm_destroy(kvq_comm_t comm);
 kvq_status kvq_compute_scales(const float *K, int64_t T, int64_t D, float *scales,
                               kvq_comm_t comm, void *stream);
 
-/* Same as kvq_compute_scales with the divisor of `fmt`: 127 (KVQ_FMT_INT8) or
- * 448 (KVQ_FMT_E4M3, the largest finite E4M3 value). */
+/* Same as kvq_compute_scales with the divisor of `fmt`: 127 (KVQ_FMT_INT8),
+ * 448 (KVQ_FMT_E4M3, the largest finite E4M3 value), 7 (KVQ_FMT_INT4) or 1
+ * (KVQ_FMT_INT2).  Unknown fmt: KVQ_ERR_INVALID_VALUE. */
 kvq_status kvq_compute_scales_fmt(const float *K, int64_t T, int64_t D, float *scales, int fmt,
                                   kvq_comm_t comm, void *stream);
 
@@ -121,6 +123,22 @@ kvq_status kvq_quantize_e4m3(const float *K, const float *scales, int64_t T, int
                              uint8_t *Kq8, float *K_hat, void *stream);
 kvq_status kvq_dequantize_e4m3(const uint8_t *Kq8, const float *scales, int64_t T, int64_t D,
                                float *K_hat, void *stream);
+
+/* INT4 / INT2 packed variant of a3 (+a4) (P:562 future work; SURVEY §8(f) NEXT-3;
+ * reading Q19), bits = 4 (qmax 7) or 2 (qmax 1):
+ *   q[t,d]     = clamp(round_half_even(fl32(K[t,d] / scales[d])), -qmax, qmax), 0 where scales[d] == 0
+ *   K_hat[t,d] = q[t,d] * scales[d]                          (if K_hat != NULL; one fp32 multiply)
+ * Kp: [T][kvq_packed_row_bytes(D, bits)] bytes out; each row packed on its own,
+ * column d's code in bits-bit two's complement at bits [bits*(d % p), +bits) of
+ * byte d / p, p = 8 / bits (low bits first); unused bits are 0.  Scales from
+ * kvq_compute_scales_fmt(KVQ_FMT_INT4 / KVQ_FMT_INT2).  Bit-identical to the
+ * oracle's kvqo_quantize_q + kvqo_pack_codes / kvqo_unpack_codes + Eq. 8.
+ * bits not in {4, 2}, NULL or aliasing buffers: KVQ_ERR_INVALID_VALUE. */
+int64_t kvq_packed_row_bytes(int64_t D, int bits); /* ceil(D * bits / 8); -1 for bad arguments */
+kvq_status kvq_quantize_packed(const float *K, const float *scales, int64_t T, int64_t D, int bits,
+                               uint8_t *Kp, float *K_hat, void *stream);
+kvq_status kvq_dequantize_packed(const uint8_t *Kp, const float *scales, int64_t T, int64_t D, int bits,
+                                 float *K_hat, void *stream);
 
 /* a3+a4 fused in one pass over K (9 B/elem instead of 10): writes both Kq and
  * K_hat, bit-identical to kvq_quantize followed by kvq_dequantize. */

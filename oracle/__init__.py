@@ -68,6 +68,10 @@ def lib():
         L.kvqo_scales_from_absmax_e4m3.argtypes = [vp, i64, vp]
         L.kvqo_quantize_e4m3.argtypes = [vp, vp, i64, i64, vp]
         L.kvqo_dequantize_e4m3.argtypes = [vp, vp, i64, i64, vp]
+        L.kvqo_scales_from_absmax_q.argtypes = [vp, i64, ctypes.c_int, vp]
+        L.kvqo_quantize_q.argtypes = [vp, vp, i64, i64, ctypes.c_int, vp]
+        L.kvqo_pack_codes.argtypes = [vp, i64, i64, ctypes.c_int, vp]
+        L.kvqo_unpack_codes.argtypes = [vp, i64, i64, ctypes.c_int, vp]
         _lib = L
     return _lib
 
@@ -221,6 +225,57 @@ def roundtrip_e4m3(K):
     s = compute_scales_e4m3(K)
     q = quantize_e4m3(K, s)
     return s, q, dequantize_e4m3(q, s)
+
+
+# --------------------------------------------------------------------------- INT4 / INT2 variant (NEXT-3)
+QMAX = {8: 127, 4: 7, 2: 1}
+
+
+def packed_row_bytes(D: int, bits: int) -> int:
+    per = 8 // bits
+    return (D + per - 1) // per
+
+
+def compute_scales_q(K, bits: int) -> np.ndarray:
+    """s_d = max_t |K[t,d]| / qmax(bits) (Alg. 1's max; reading Q19)."""
+    K = _f32(K)
+    m = np.zeros(K.shape[1], dtype=np.float32)
+    absmax_rows(K, m)
+    s = np.empty_like(m)
+    lib().kvqo_scales_from_absmax_q(_p(m), m.shape[0], QMAX[bits], _p(s))
+    return s
+
+
+def quantize_q(K, scales, bits: int) -> np.ndarray:
+    """Unpacked int8 codes in [-qmax, qmax]."""
+    K, scales = _f32(K), _f32(scales)
+    T, D = K.shape
+    q = np.empty((T, D), dtype=np.int8)
+    lib().kvqo_quantize_q(_p(K), _p(scales), T, D, QMAX[bits], _p(q))
+    return q
+
+
+def pack_codes(q, bits: int) -> np.ndarray:
+    q = np.ascontiguousarray(q, dtype=np.int8)
+    T, D = q.shape
+    out = np.empty((T, packed_row_bytes(D, bits)), dtype=np.uint8)
+    lib().kvqo_pack_codes(_p(q), T, D, bits, _p(out))
+    return out
+
+
+def unpack_codes(p, D: int, bits: int) -> np.ndarray:
+    p = np.ascontiguousarray(p, dtype=np.uint8)
+    T = p.shape[0]
+    q = np.empty((T, D), dtype=np.int8)
+    lib().kvqo_unpack_codes(_p(p), T, D, bits, _p(q))
+    return q
+
+
+def roundtrip_q(K, bits: int):
+    """scales, packed codes, reconstruction (Eq. 8 on the unpacked codes)."""
+    s = compute_scales_q(K, bits)
+    q = quantize_q(K, s, bits)
+    return s, pack_codes(q, bits), dequantize(q, s)
 
 
 # --------------------------------------------------------------------------- whole pipeline

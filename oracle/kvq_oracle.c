@@ -30,6 +30,11 @@
  *                                    pinned: hand-worked E4M3 codes incl. ties and saturation,
  *                                    torch float8_e4m3fn on all 256 codes and exhaustively over
  *                                    every fp32 in [2^-12, 448), numpy abs-max / 448
+ *   kvqo_scales_from_absmax_q, kvqo_quantize_q, kvqo_pack_codes / kvqo_unpack_codes
+ *   (NEXT-3 INT4 / INT2)             pinned: hand-worked codes and packed bytes, numpy
+ *                                    rint(fp32(K/s)) clip, exact-rational brute force, pack /
+ *                                    unpack round trip vs numpy bit arithmetic, error bound s/2,
+ *                                    qmax = 127 reduces to kvqo_quantize
  *   No function is "parity unpinned".
  */
 #include <math.h>
@@ -310,4 +315,72 @@ void kvqo_dequantize_e4m3(const uint8_t *Kq, const float *scales, int64_t T, int
     for (int64_t t = 0; t < T; t++)
         for (int64_t d = 0; d < D; d++)
             K_hat[t * D + d] = kvqo_e4m3_decode(Kq[t * D + d]) * scales[d];
+}
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-3: INT4 / INT2 per-channel variant (future work P:562; reading Q19).  */
+/* The same method with a smaller symmetric code range [-qmax, qmax]:         */
+/* qmax = 7 (4-bit) or 1 (2-bit); everything else as Eq. 6-8.                */
+/* ------------------------------------------------------------------------ */
+
+/* Alg. 1's last line with the divisor qmax: s_d = max_abs / qmax (fp32 division). */
+void kvqo_scales_from_absmax_q(const float *max_abs, int64_t D, int qmax, float *scales)
+{
+    for (int64_t d = 0; d < D; d++)
+        scales[d] = max_abs[d] / (float)qmax;
+}
+
+/* Eq. 7 with the clamp at +-qmax: q = clamp(rint(fl32(K/s)), -qmax, qmax), 0 where s == 0. */
+void kvqo_quantize_q(const float *K, const float *scales, int64_t T, int64_t D, int qmax, int8_t *q)
+{
+    for (int64_t t = 0; t < T; t++) {
+        for (int64_t d = 0; d < D; d++) {
+            float s = scales[d];
+            int c;
+            if (s == 0.0f) {
+                c = 0;
+            } else {
+                float v = K[t * D + d] / s;
+                float r = rintf(v);
+                if (r > (float)qmax)
+                    r = (float)qmax;
+                if (r < -(float)qmax)
+                    r = -(float)qmax;
+                c = (int)r;
+            }
+            q[t * D + d] = (int8_t)c;
+        }
+    }
+}
+
+/* Storage (reading Q19): each row packed on its own into ceil(D * bits / 8)
+ * bytes; column d's code, in `bits`-bit two's complement, occupies bits
+ * [bits * (d % per), bits * (d % per) + bits) of byte d / per, per = 8 / bits
+ * (low bits first: column 2j in the low nibble for INT4); unused bits are 0. */
+void kvqo_pack_codes(const int8_t *q, int64_t T, int64_t D, int bits, uint8_t *out)
+{
+    int per = 8 / bits;
+    int64_t rb = (D + per - 1) / per;
+    unsigned mask = (1u << bits) - 1u;
+    for (int64_t t = 0; t < T; t++) {
+        for (int64_t j = 0; j < rb; j++)
+            out[t * rb + j] = 0;
+        for (int64_t d = 0; d < D; d++) {
+            unsigned field = ((unsigned)(int)q[t * D + d]) & mask;
+            out[t * rb + d / per] |= (uint8_t)(field << (bits * (int)(d % per)));
+        }
+    }
+}
+
+void kvqo_unpack_codes(const uint8_t *in, int64_t T, int64_t D, int bits, int8_t *q)
+{
+    int per = 8 / bits;
+    int64_t rb = (D + per - 1) / per;
+    unsigned mask = (1u << bits) - 1u;
+    for (int64_t t = 0; t < T; t++)
+        for (int64_t d = 0; d < D; d++) {
+            unsigned field = ((unsigned)in[t * rb + d / per] >> (bits * (int)(d % per))) & mask;
+            int c = (field & (1u << (bits - 1))) ? (int)field - (1 << bits) : (int)field;
+            q[t * D + d] = (int8_t)c;
+        }
 }

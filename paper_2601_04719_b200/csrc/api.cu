@@ -132,7 +132,8 @@ extern "C" kvq_status kvq_compute_scales_fmt(const float *K, int64_t T, int64_t 
                                              kvq_comm_t comm, void *stream) {
     KVQ_REQUIRE(K && scales, "kvq_compute_scales: NULL pointer");
     KVQ_REQUIRE(!bad_dims(T, D), "kvq_compute_scales: need T >= 1, D >= 1, T*D <= 2^62");
-    KVQ_REQUIRE(fmt == KVQ_FMT_INT8 || fmt == KVQ_FMT_E4M3, "kvq_compute_scales: unknown format");
+    KVQ_REQUIRE(fmt == KVQ_FMT_INT8 || fmt == KVQ_FMT_E4M3 || fmt == KVQ_FMT_INT4 || fmt == KVQ_FMT_INT2,
+                "kvq_compute_scales: unknown format");
     KVQ_REQUIRE(!overlap(K, (size_t)(T * D) * 4, scales, (size_t)D * 4), "kvq_compute_scales: scales aliases K");
     KVQ_TRY(device_ok());
     cudaStream_t s = (cudaStream_t)stream;
@@ -140,7 +141,8 @@ extern "C" kvq_status kvq_compute_scales_fmt(const float *K, int64_t T, int64_t 
     KVQ_TRY(cuda_check(cudaMemsetAsync(bits, 0, (size_t)D * 4, s), "memset scales"));
     KVQ_TRY(launch_colmax(K, T, D, bits, s));
     if (comm) KVQ_TRY(comm_allreduce_max_u32(comm, bits, (size_t)D, s));
-    return launch_finalize(bits, D, s, fmt == KVQ_FMT_E4M3 ? 448.0f : 127.0f);
+    const float divisor = fmt == KVQ_FMT_E4M3 ? 448.0f : fmt == KVQ_FMT_INT4 ? 7.0f : fmt == KVQ_FMT_INT2 ? 1.0f : 127.0f;
+    return launch_finalize(bits, D, s, divisor);
 }
 
 extern "C" kvq_status kvq_compute_scales(const float *K, int64_t T, int64_t D, float *scales, kvq_comm_t comm,
@@ -173,6 +175,40 @@ extern "C" kvq_status kvq_dequantize_e4m3(const uint8_t *Kq8, const float *scale
                 "kvq_dequantize_e4m3: K_hat aliases an input");
     KVQ_TRY(device_ok());
     return launch_dequantize_e4m3(Kq8, scales, T, D, K_hat, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------------------ INT4 / INT2 packed (NEXT-3)
+extern "C" int64_t kvq_packed_row_bytes(int64_t D, int bits) {
+    if (D < 1 || (bits != 4 && bits != 2)) return -1;
+    return packed_row_bytes(D, bits);
+}
+
+extern "C" kvq_status kvq_quantize_packed(const float *K, const float *scales, int64_t T, int64_t D, int bits,
+                                          uint8_t *Kp, float *K_hat, void *stream) {
+    KVQ_REQUIRE(K && scales && Kp, "kvq_quantize_packed: NULL pointer");
+    KVQ_REQUIRE(bits == 4 || bits == 2, "kvq_quantize_packed: bits must be 4 or 2");
+    KVQ_REQUIRE(!bad_dims(T, D), "kvq_quantize_packed: need T >= 1, D >= 1, T*D <= 2^62");
+    const size_t n = (size_t)(T * D), np = (size_t)(T * packed_row_bytes(D, bits));
+    KVQ_REQUIRE(!overlap(K, n * 4, Kp, np) && !overlap(scales, (size_t)D * 4, Kp, np),
+                "kvq_quantize_packed: Kp aliases an input");
+    if (K_hat)
+        KVQ_REQUIRE(!overlap(K_hat, n * 4, K, n * 4) && !overlap(K_hat, n * 4, Kp, np) &&
+                        !overlap(K_hat, n * 4, scales, (size_t)D * 4),
+                    "kvq_quantize_packed: K_hat aliases an input");
+    KVQ_TRY(device_ok());
+    return launch_quantize_packed(K, scales, T, D, bits, Kp, K_hat, (cudaStream_t)stream);
+}
+
+extern "C" kvq_status kvq_dequantize_packed(const uint8_t *Kp, const float *scales, int64_t T, int64_t D, int bits,
+                                            float *K_hat, void *stream) {
+    KVQ_REQUIRE(Kp && scales && K_hat, "kvq_dequantize_packed: NULL pointer");
+    KVQ_REQUIRE(bits == 4 || bits == 2, "kvq_dequantize_packed: bits must be 4 or 2");
+    KVQ_REQUIRE(!bad_dims(T, D), "kvq_dequantize_packed: need T >= 1, D >= 1, T*D <= 2^62");
+    const size_t n = (size_t)(T * D), np = (size_t)(T * packed_row_bytes(D, bits));
+    KVQ_REQUIRE(!overlap(K_hat, n * 4, Kp, np) && !overlap(K_hat, n * 4, scales, (size_t)D * 4),
+                "kvq_dequantize_packed: K_hat aliases an input");
+    KVQ_TRY(device_ok());
+    return launch_dequantize_packed(Kp, scales, T, D, bits, K_hat, (cudaStream_t)stream);
 }
 
 // ------------------------------------------------------------------------------ a3, a4

@@ -43,6 +43,12 @@ kvq_status launch_quantize_e4m3(const float *K, const float *scales, int64_t T, 
                                 float *K_hat /* nullable */, cudaStream_t s);
 kvq_status launch_dequantize_e4m3(const uint8_t *Kq, const float *scales, int64_t T, int64_t D, float *K_hat,
                                   cudaStream_t s);
+// ---- INT4 / INT2 packed variant (lowbit_kernels.cu)
+int64_t packed_row_bytes(int64_t D, int bits);
+kvq_status launch_quantize_packed(const float *K, const float *scales, int64_t T, int64_t D, int bits, uint8_t *Kp,
+                                  float *K_hat /* nullable */, cudaStream_t s);
+kvq_status launch_dequantize_packed(const uint8_t *Kp, const float *scales, int64_t T, int64_t D, int bits,
+                                    float *K_hat, cudaStream_t s);
 kvq_status launch_quantize(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
                            float *K_hat /* nullable: fused a3+a4 */, cudaStream_t s);
 kvq_status launch_dequantize(const int8_t *Kq, const float *scales, int64_t T, int64_t D, float *K_hat,

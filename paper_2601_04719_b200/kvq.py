@@ -20,6 +20,7 @@ __all__ = [
     "kvq_comm_unique_id", "METRICS_BYTES", "metrics_from_device", "kvq_roundtrip", "kvq_roundtrip_workspace_size",
     "kvq_quantize_fused", "kvq_roundtrip_host_async", "metrics_from_host", "kvq_compute_scales_fmt",
     "kvq_quantize_e4m3", "kvq_dequantize_e4m3", "FMT_INT8", "FMT_E4M3", "kvq_scores_from_codes",
+    "FMT_INT4", "FMT_INT2", "kvq_packed_row_bytes", "kvq_quantize_packed", "kvq_dequantize_packed",
 ]
 
 load()  # fail loudly at import if libkvq.so cannot be loaded or built
@@ -104,7 +105,7 @@ def kvq_compute_scales(K: torch.Tensor, scales: Optional[torch.Tensor] = None, c
     return scales
 
 
-FMT_INT8, FMT_E4M3 = 0, 1
+FMT_INT8, FMT_E4M3, FMT_INT4, FMT_INT2 = 0, 1, 2, 3
 
 
 def kvq_compute_scales_fmt(K: torch.Tensor, fmt: int, scales: Optional[torch.Tensor] = None,
@@ -140,6 +141,44 @@ def kvq_dequantize_e4m3(Kq8: torch.Tensor, scales: torch.Tensor, K_hat: Optional
         K_hat = torch.empty((T, D), dtype=torch.float32, device=Kq8.device)
     check(load().kvq_dequantize_e4m3(_ptr(Kq8), _ptr(scales), T, D, _ptr(K_hat), _stream(stream)),
           "kvq_dequantize_e4m3")
+    return K_hat
+
+
+def kvq_packed_row_bytes(D: int, bits: int) -> int:
+    n = int(load().kvq_packed_row_bytes(D, bits))
+    if n < 0:
+        raise ValueError(f"kvq_packed_row_bytes: bad D={D} or bits={bits}")
+    return n
+
+
+def kvq_quantize_packed(K: torch.Tensor, scales: torch.Tensor, bits: int, Kp: Optional[torch.Tensor] = None,
+                        K_hat: Optional[torch.Tensor] = None, want_khat: bool = False, stream=None):
+    """INT4 (bits=4) / INT2 (bits=2) codes packed per row (uint8 [T][ceil(D*bits/8)]);
+    also K_hat when given or want_khat."""
+    T, D = _mat(K, torch.float32, "K")
+    _vec(scales, D, "scales")
+    rb = kvq_packed_row_bytes(D, bits)
+    if Kp is None:
+        Kp = torch.empty((T, rb), dtype=torch.uint8, device=K.device)
+    if Kp.dtype != torch.uint8 or tuple(Kp.shape) != (T, rb) or not Kp.is_contiguous() or not Kp.is_cuda:
+        raise ValueError(f"Kp: expected contiguous CUDA uint8[{T}, {rb}]")
+    if K_hat is None and want_khat:
+        K_hat = torch.empty((T, D), dtype=torch.float32, device=K.device)
+    check(load().kvq_quantize_packed(_ptr(K), _ptr(scales), T, D, bits, _ptr(Kp), _ptr(K_hat), _stream(stream)),
+          "kvq_quantize_packed")
+    return (Kp, K_hat) if K_hat is not None else Kp
+
+
+def kvq_dequantize_packed(Kp: torch.Tensor, scales: torch.Tensor, D: int, bits: int,
+                          K_hat: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    T, rb = _mat(Kp, torch.uint8, "Kp")
+    if rb != kvq_packed_row_bytes(D, bits):
+        raise ValueError(f"Kp: {rb} bytes per row, expected {kvq_packed_row_bytes(D, bits)} for D={D}, bits={bits}")
+    _vec(scales, D, "scales")
+    if K_hat is None:
+        K_hat = torch.empty((T, D), dtype=torch.float32, device=Kp.device)
+    check(load().kvq_dequantize_packed(_ptr(Kp), _ptr(scales), T, D, bits, _ptr(K_hat), _stream(stream)),
+          "kvq_dequantize_packed")
     return K_hat
 
 

@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""NEXT-1 fidelity comparison: INT8 (the paper's method) vs FP8 E4M3 per-channel
+"""NEXT-1 / NEXT-3 fidelity comparison: INT8 (the paper's method) vs FP8 E4M3, INT4 and INT2 per-channel
 quantization of the same key matrices, through the same fidelity checks (a5, a6:
 L2, max-abs, mean |Q.K^T - Q.K_hat^T| with nq = 64).  Both paths are parity-tested
 bit-exact against the oracle (tests/test_gpu_parity.py, tests/test_gpu_fp8.py);
@@ -28,7 +28,13 @@ for name, (T, D) in CONFIGS.items():
         sf = kvq.kvq_compute_scales_fmt(K, kvq.FMT_E4M3)
         qf, khf = kvq.kvq_quantize_e4m3(K, sf, want_khat=True)
         res["e4m3"] = kvq.kvq_error_metrics(K, khf, Q, sf)
-        del qf, khf, K
+        del qf, khf
+        for bits, fmt in ((4, kvq.FMT_INT4), (2, kvq.FMT_INT2)):
+            sb = kvq.kvq_compute_scales_fmt(K, fmt)
+            pb, khb = kvq.kvq_quantize_packed(K, sb, bits, want_khat=True)
+            res[f"int{bits}"] = kvq.kvq_error_metrics(K, khb, Q, sb)
+            del pb, khb
+        del K
         torch.cuda.empty_cache()
         row[dname] = {fmt: {k: m[k] for k in ("l2", "max_abs", "attn_mean_abs")} for fmt, m in res.items()}
     out[name] = {"T": T, "D": D, **row}
