@@ -140,6 +140,30 @@ kvq_status kvq_quantize_packed(const float *K, const float *scales, int64_t T, i
 kvq_status kvq_dequantize_packed(const uint8_t *Kp, const float *scales, int64_t T, int64_t D, int bits,
                                  float *K_hat, void *stream);
 
+/* NEXT-4 (P:564 dynamic quantization, P:570 persistent kernels;
+ * reading Q20): append n_new tokens to a growing key cache with dynamic
+ * per-channel scales, keeping streaming == batch BIT FOR BIT:
+ *   after the call, scales == kvq_compute_scales(K[0:T_new]) and
+ *   Kq[0:T_new] (and K_hat[0:T_new]) == kvq_quantize(_dequantize)(K[0:T_new], scales),
+ *   T_new = T_old + n_new.
+ * K:      [T_new][D] fp32 [device], the retained full-precision cache; rows
+ *         [T_old, T_new) hold the new tokens (written by the caller).  Read only.
+ * absmax: [D] uint32 [device] running column abs-max (IEEE bits of |x|), and
+ * scales: [D] fp32 [device] running scales: both zero-filled by the caller
+ *         before the first append, then owned by this call.
+ * Kq:     [T_new][D] int8 [device]; K_hat: [T_new][D] fp32 [device] or NULL.
+ * Codes of old rows are rewritten only in columns whose scale changed
+ * ("re-quantize when a scale grows").  n_new may be 0 (T_old >= 0).
+ * comm != NULL: token-sharded cache; every rank calls with its own shard and
+ * its own n_new (0 allowed); the running max is all-reduced (MAX) each call,
+ * so scales stay global.  Decode-sized appends (n_new <= 256, comm == NULL)
+ * run as ONE cooperative launch.  workspace: kvq_append_workspace_size(D)
+ * bytes [device], not shared by concurrent calls. */
+size_t kvq_append_workspace_size(int64_t D);
+kvq_status kvq_append(const float *K, int64_t T_old, int64_t n_new, int64_t D, uint32_t *absmax,
+                      float *scales, int8_t *Kq, float *K_hat, void *workspace, size_t workspace_bytes,
+                      kvq_comm_t comm, void *stream);
+
 /* a3+a4 fused in one pass over K (9 B/elem instead of 10): writes both Kq and
  * K_hat, bit-identical to kvq_quantize followed by kvq_dequantize. */
 kvq_status kvq_quantize_dequantize(const float *K, const float *scales, int64_t T, int64_t D,

@@ -42,6 +42,8 @@ SIGNATURES = {
     "kvq_compute_scales_fmt": (_int, [_vp, _i64, _i64, _vp, _int, _vp, _vp]),
     "kvq_quantize_e4m3": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "kvq_dequantize_e4m3": (_int, [_vp, _vp, _i64, _i64, _vp, _vp]),
+    "kvq_append_workspace_size": (_sz, [_i64]),
+    "kvq_append": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
     "kvq_packed_row_bytes": (_i64, [_i64, _int]),
     "kvq_quantize_packed": (_int, [_vp, _vp, _i64, _i64, _int, _vp, _vp, _vp]),
     "kvq_dequantize_packed": (_int, [_vp, _vp, _i64, _i64, _int, _vp, _vp]),

@@ -177,6 +177,29 @@ extern "C" kvq_status kvq_dequantize_e4m3(const uint8_t *Kq8, const float *scale
     return launch_dequantize_e4m3(Kq8, scales, T, D, K_hat, (cudaStream_t)stream);
 }
 
+// ------------------------------------------------------------------------------ streaming append (NEXT-4)
+extern "C" size_t kvq_append_workspace_size(int64_t D) { return D < 1 ? 0 : append_workspace_size(D); }
+
+extern "C" kvq_status kvq_append(const float *K, int64_t T_old, int64_t n_new, int64_t D, uint32_t *absmax,
+                                 float *scales, int8_t *Kq, float *K_hat, void *workspace, size_t workspace_bytes,
+                                 kvq_comm_t comm, void *stream) {
+    KVQ_REQUIRE(K && absmax && scales && Kq && workspace, "kvq_append: NULL pointer");
+    KVQ_REQUIRE(T_old >= 0 && n_new >= 0 && D >= 1, "kvq_append: need T_old >= 0, n_new >= 0, D >= 1");
+    const int64_t T = T_old + n_new;
+    KVQ_REQUIRE(T >= 1 && !bad_dims(T, D), "kvq_append: need T_old + n_new >= 1 and (T_old + n_new) * D <= 2^62");
+    KVQ_REQUIRE(workspace_bytes >= append_workspace_size(D), "kvq_append: workspace too small");
+    const size_t n = (size_t)(T * D), d4 = (size_t)D * 4;
+    KVQ_REQUIRE(!overlap(K, n * 4, Kq, n) && !overlap(K, n * 4, absmax, d4) && !overlap(K, n * 4, scales, d4) &&
+                    !overlap(absmax, d4, scales, d4) && !overlap(Kq, n, scales, d4) && !overlap(Kq, n, absmax, d4),
+                "kvq_append: buffers alias");
+    if (K_hat)
+        KVQ_REQUIRE(!overlap(K_hat, n * 4, K, n * 4) && !overlap(K_hat, n * 4, Kq, n) &&
+                        !overlap(K_hat, n * 4, scales, d4) && !overlap(K_hat, n * 4, absmax, d4),
+                    "kvq_append: K_hat aliases an input");
+    KVQ_TRY(device_ok());
+    return launch_append(K, T_old, n_new, D, absmax, scales, Kq, K_hat, workspace, comm, (cudaStream_t)stream);
+}
+
 // ------------------------------------------------------------------------------ INT4 / INT2 packed (NEXT-3)
 extern "C" int64_t kvq_packed_row_bytes(int64_t D, int bits) {
     if (D < 1 || (bits != 4 && bits != 2)) return -1;

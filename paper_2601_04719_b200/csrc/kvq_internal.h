@@ -43,6 +43,10 @@ kvq_status launch_quantize_e4m3(const float *K, const float *scales, int64_t T, 
                                 float *K_hat /* nullable */, cudaStream_t s);
 kvq_status launch_dequantize_e4m3(const uint8_t *Kq, const float *scales, int64_t T, int64_t D, float *K_hat,
                                   cudaStream_t s);
+// ---- streaming append with dynamic scales (append_kernels.cu, NEXT-4)
+size_t append_workspace_size(int64_t D);
+kvq_status launch_append(const float *K, int64_t T_old, int64_t n_new, int64_t D, uint32_t *absmax, float *scales,
+                         int8_t *Kq, float *K_hat, void *ws, kvq_comm_t comm, cudaStream_t s);
 // ---- INT4 / INT2 packed variant (lowbit_kernels.cu)
 int64_t packed_row_bytes(int64_t D, int bits);
 kvq_status launch_quantize_packed(const float *K, const float *scales, int64_t T, int64_t D, int bits, uint8_t *Kp,

@@ -21,6 +21,7 @@ __all__ = [
     "kvq_quantize_fused", "kvq_roundtrip_host_async", "metrics_from_host", "kvq_compute_scales_fmt",
     "kvq_quantize_e4m3", "kvq_dequantize_e4m3", "FMT_INT8", "FMT_E4M3", "kvq_scores_from_codes",
     "FMT_INT4", "FMT_INT2", "kvq_packed_row_bytes", "kvq_quantize_packed", "kvq_dequantize_packed",
+    "kvq_append", "kvq_append_workspace_size", "AppendCache",
 ]
 
 load()  # fail loudly at import if libkvq.so cannot be loaded or built
@@ -142,6 +143,58 @@ def kvq_dequantize_e4m3(Kq8: torch.Tensor, scales: torch.Tensor, K_hat: Optional
     check(load().kvq_dequantize_e4m3(_ptr(Kq8), _ptr(scales), T, D, _ptr(K_hat), _stream(stream)),
           "kvq_dequantize_e4m3")
     return K_hat
+
+
+def kvq_append_workspace_size(D: int) -> int:
+    return int(load().kvq_append_workspace_size(D))
+
+
+def kvq_append(K: torch.Tensor, T_old: int, n_new: int, absmax: torch.Tensor, scales: torch.Tensor,
+               Kq: torch.Tensor, K_hat: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+               comm: Optional["Comm"] = None, stream=None) -> None:
+    """NEXT-4: rows [T_old, T_old + n_new) of K are new tokens; update the running
+    column max / scales and the codes (and K_hat) so they equal the batch method on
+    K[0:T_old + n_new].  K, Kq, K_hat may have more rows (capacity) than T_old + n_new."""
+    cap, D = _mat(K, torch.float32, "K")
+    if T_old < 0 or n_new < 0 or T_old + n_new > cap:
+        raise ValueError(f"kvq_append: rows [{T_old}, {T_old + n_new}) exceed the capacity {cap}")
+    if absmax.dtype != torch.int32 or absmax.numel() != D or not absmax.is_cuda or not absmax.is_contiguous():
+        raise ValueError(f"absmax: expected contiguous CUDA int32[{D}] (uint32 bit patterns)")
+    _vec(scales, D, "scales")
+    if _mat(Kq, torch.int8, "Kq") [1] != D or Kq.shape[0] < T_old + n_new:
+        raise ValueError("Kq: expected int8 [>= T_old + n_new, D]")
+    if K_hat is not None and (_mat(K_hat, torch.float32, "K_hat")[1] != D or K_hat.shape[0] < T_old + n_new):
+        raise ValueError("K_hat: expected float32 [>= T_old + n_new, D]")
+    if workspace is None:
+        workspace = torch.empty(kvq_append_workspace_size(D), dtype=torch.uint8, device=K.device)
+    check(load().kvq_append(_ptr(K), T_old, n_new, D, _ptr(absmax), _ptr(scales), _ptr(Kq), _ptr(K_hat),
+                            _ptr(workspace), workspace.numel(), _comm_handle(comm), _stream(stream)), "kvq_append")
+
+
+class AppendCache:
+    """Device buffers of a growing key cache (capacity rows x D): retained fp32 K,
+    int8 codes, optional K_hat, and the running absmax / scales state that
+    kvq_append maintains.  Plumbing only; every step runs in kvq_append."""
+
+    def __init__(self, capacity: int, D: int, keep_khat: bool = True, device="cuda", comm=None):
+        self.D, self.T, self.comm = D, 0, comm
+        self.K = torch.empty((capacity, D), dtype=torch.float32, device=device)
+        self.Kq = torch.empty((capacity, D), dtype=torch.int8, device=device)
+        self.K_hat = torch.empty((capacity, D), dtype=torch.float32, device=device) if keep_khat else None
+        self.absmax = torch.zeros(D, dtype=torch.int32, device=device)
+        self.scales = torch.zeros(D, dtype=torch.float32, device=device)
+        self.ws = torch.empty(kvq_append_workspace_size(D), dtype=torch.uint8, device=device)
+
+    def append(self, rows: Optional[torch.Tensor], stream=None) -> None:
+        n = 0 if rows is None else rows.shape[0]
+        if n:
+            if stream is not None:
+                with torch.cuda.stream(stream):
+                    self.K[self.T:self.T + n].copy_(rows, non_blocking=True)
+            else:
+                self.K[self.T:self.T + n].copy_(rows, non_blocking=True)
+        kvq_append(self.K, self.T, n, self.absmax, self.scales, self.Kq, self.K_hat, self.ws, self.comm, stream)
+        self.T += n
 
 
 def kvq_packed_row_bytes(D: int, bits: int) -> int:

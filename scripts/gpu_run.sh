@@ -1,7 +1,5 @@
-for f in int4 int2; do timeout 300 python bench.py --format $f --steps 50 --warmup 5 > gpurun_out/bench_$f.json 2> gpurun_out/bench_$f.err; tail -2 gpurun_out/bench_$f.err; done
-python - <<'PY'
+timeout 600 python scripts/bench_append.py > gpurun_out/bench_append.json 2> gpurun_out/bench_append.err; tail -3 gpurun_out/bench_append.err
+python -c "
 import json
-for f in ("int4","int2"):
-    d=json.loads(open(f"gpurun_out/bench_{f}.json").read().strip().splitlines()[-1])
-    print(f, d["ms_per_step"], {k:(round(v["ms"],3), round(v["frac_hbm"],3)) for k,v in d["passes"].items()})
-PY
+for r in json.load(open('gpurun_out/bench_append.json')): print(r)
+"

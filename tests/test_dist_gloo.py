@@ -108,3 +108,54 @@ def test_shard_rows_partition(world, T):
     assert max(n for _, n in spans) - min(n for _, n in spans) <= 1
     with pytest.raises(ValueError):
         shard_rows(T, world, world)
+
+
+def _append_worker(rank, world, port, D, steps, out_dir):
+    """NEXT-4 on a token-sharded cache: every rank appends its own tokens each
+    step (0 allowed), the running column max is all-reduced (MAX) each step, and a
+    rank re-quantizes its old rows in columns whose global scale changed -- the
+    algorithm kvq_append runs with a communicator, with the oracle as the kernels."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(100 + rank)
+        K = np.zeros((0, D), np.float32)
+        absmax = np.zeros(D, np.float32)
+        scales = np.zeros(D, np.float32)
+        codes = np.zeros((0, D), np.int8)
+        for step, n in enumerate(steps[rank]):
+            new = (oracle.fill(n, D, 1000 + 10 * step + rank, 1) * (1.0 + step)).astype(np.float32)
+            K = np.concatenate([K, new])
+            oracle.absmax_rows(new, absmax)  # phase A on this rank's new rows
+            bits = torch.from_numpy(absmax.view(np.int32).copy())
+            dist.all_reduce(bits, op=dist.ReduceOp.MAX)
+            absmax = bits.numpy().view(np.float32).copy()
+            s_new = oracle.scales_from_absmax(absmax)  # phase B
+            grown = s_new.view(np.uint32) != scales.view(np.uint32)
+            scales = s_new
+            if codes.shape[0] and grown.any():  # phase C: old rows of grown columns
+                codes[:, grown] = oracle.quantize(K[:codes.shape[0]][:, grown], scales[grown])
+            codes = np.concatenate([codes, oracle.quantize(new, scales)]) if n else codes
+        np.save(os.path.join(out_dir, f"app_K{rank}.npy"), K)
+        np.save(os.path.join(out_dir, f"app_q{rank}.npy"), codes)
+        np.save(os.path.join(out_dir, f"app_s{rank}.npy"), scales)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_append_sharded_equals_batch(tmp_path):
+    import oracle
+    D = 24
+    steps = [[5, 1, 0, 3, 1, 7], [2, 0, 4, 1, 1, 9]]
+    mp.spawn(_append_worker, args=(2, _free_port(), D, steps, str(tmp_path)), nprocs=2, join=True)
+    Ks = [np.load(tmp_path / f"app_K{r}.npy") for r in range(2)]
+    s0, s1 = (np.load(tmp_path / f"app_s{r}.npy") for r in range(2))
+    assert np.array_equal(s0.view(np.uint32), s1.view(np.uint32))
+    batch_s = oracle.compute_scales(np.concatenate(Ks))  # the unsharded batch method over all tokens
+    assert np.array_equal(s0.view(np.uint32), batch_s.view(np.uint32))
+    for r in range(2):
+        assert np.array_equal(np.load(tmp_path / f"app_q{r}.npy"), oracle.quantize(Ks[r], batch_s))
