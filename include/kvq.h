@@ -153,7 +153,8 @@ kvq_status kvq_dequantize_packed(const uint8_t *Kp, const float *scales, int64_t
  *         before the first append, then owned by this call.
  * Kq:     [T_new][D] int8 [device]; K_hat: [T_new][D] fp32 [device] or NULL.
  * Codes of old rows are rewritten only in columns whose scale changed
- * ("re-quantize when a scale grows").  n_new may be 0 (T_old >= 0).
+ * ("re-quantize when a scale grows").  n_new may be 0 and T_old may be 0 (an
+ * empty append still takes part in the all-reduce when comm != NULL).
  * comm != NULL: token-sharded cache; every rank calls with its own shard and
  * its own n_new (0 allowed); the running max is all-reduced (MAX) each call,
  * so scales stay global.  Decode-sized appends (n_new <= 256, comm == NULL)

@@ -186,7 +186,7 @@ extern "C" kvq_status kvq_append(const float *K, int64_t T_old, int64_t n_new, i
     KVQ_REQUIRE(K && absmax && scales && Kq && workspace, "kvq_append: NULL pointer");
     KVQ_REQUIRE(T_old >= 0 && n_new >= 0 && D >= 1, "kvq_append: need T_old >= 0, n_new >= 0, D >= 1");
     const int64_t T = T_old + n_new;
-    KVQ_REQUIRE(T >= 1 && !bad_dims(T, D), "kvq_append: need T_old + n_new >= 1 and (T_old + n_new) * D <= 2^62");
+    KVQ_REQUIRE(T == 0 || !bad_dims(T, D), "kvq_append: need (T_old + n_new) * D <= 2^62");
     KVQ_REQUIRE(workspace_bytes >= append_workspace_size(D), "kvq_append: workspace too small");
     const size_t n = (size_t)(T * D), d4 = (size_t)D * 4;
     KVQ_REQUIRE(!overlap(K, n * 4, Kq, n) && !overlap(K, n * 4, absmax, d4) && !overlap(K, n * 4, scales, d4) &&

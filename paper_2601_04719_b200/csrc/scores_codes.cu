@@ -197,7 +197,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     }
     if (warp == 1) tmem_alloc_pair<TMEM_COLS>(&s.tmem_base);
     tc_fence_before();
-    cluster_sync();
+    __syncthreads();  // CTA-local order of the alloc's smem write (racecheck models bar.sync, not barrier.cluster)
+    cluster_sync();   // peer barriers initialised before any remote arrive / TMA complete_tx
     tc_fence_after();
     const uint32_t tbase = s.tmem_base;
 

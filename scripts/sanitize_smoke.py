@@ -22,4 +22,20 @@ for (T, D, nq) in [(300, 64, 7), (129, 48, 64), (77, 13, 5), (1, 4, 1), (257, 10
     r = kvq.kvq_roundtrip_host(K.cpu().pin_memory(), Q.cpu().pin_memory())
     torch.cuda.synchronize()
     assert torch.equal(q, q2) and torch.equal(q, q3) and torch.equal(q, q4)
+    # NEXT rows: FP8, INT4/INT2 packed, scores from codes (int8 tensor cores, CTA pairs), streaming append
+    sf = kvq.kvq_compute_scales_fmt(K, kvq.FMT_E4M3)
+    q8, kh8 = kvq.kvq_quantize_e4m3(K, sf, want_khat=True)
+    kh8b = kvq.kvq_dequantize_e4m3(q8, sf)
+    for bits, fmt in ((4, kvq.FMT_INT4), (2, kvq.FMT_INT2)):
+        sb = kvq.kvq_compute_scales_fmt(K, fmt)
+        pb, khb = kvq.kvq_quantize_packed(K, sb, bits, want_khat=True)
+        khb2 = kvq.kvq_dequantize_packed(pb, sb, D, bits)
+        assert torch.equal(khb, khb2)
+    if nq <= 64:
+        Sc = kvq.kvq_scores_from_codes(Q, q, s)
+    cache = kvq.AppendCache(T + 8, D)
+    cache.append(K[: T // 2])
+    cache.append(K[T // 2: T // 2 + 1] * 3.0)
+    cache.append(K[T // 2 + 1: T])
+    torch.cuda.synchronize()
     print(T, D, nq, "ok", m["attn_mean_abs"], single)
