@@ -65,7 +65,7 @@ def peaks():
 class ClockSampler:
     QUERY = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,clocks.mem")
 
     def __init__(self, index: int):
         self.index = index
@@ -97,7 +97,7 @@ class ClockSampler:
         """Median SM clock and active throttle reasons over the samples taken
         inside the wall-clock window [t0, t1] (the timed region)."""
         import datetime
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, mem, pw = [], None, set(), [], []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for l in getattr(self, "lines", []):
             f = [x.strip() for x in l.split(",")]
@@ -112,11 +112,18 @@ class ClockSampler:
                 continue
             sm.append(clk)
             mx = cmax
+            try:
+                pw.append(float(f[4]))
+                if len(f) > 10:
+                    mem.append(float(f[10]))
+            except ValueError:
+                pass
             for n, v in zip(names, f[6:10]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "mem_mhz": statistics.median(mem) if mem else None,
+                "power_w": statistics.median(pw) if pw else None}
 
 
 # ----------------------------------------------------------------------------- CPU oracle (baseline / reference arm)

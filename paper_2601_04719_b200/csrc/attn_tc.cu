@@ -76,6 +76,14 @@ struct __align__(16) ColRec {
     uint32_t pad[3];
 };
 
+// Waits on the critical path (MMA issuer, converters): a tight try_wait loop, or
+// the hardware-suspending variant when built with -DKVQ_SLEEP_ALL.
+#ifdef KVQ_SLEEP_ALL
+#define KVQ_WAIT_HOT mbar_wait_sleep
+#else
+#define KVQ_WAIT_HOT mbar_wait
+#endif
+
 struct __align__(1024) Smem {
     // modes 0/1: stage i = [K box | K_hat box] at 32 KB * i (4 stages)
     // fused:     stage i = K box at 16 KB * i (8 stages; the converters overwrite it in place with
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nkb; kb++, g++) {
                     const int sk = g % KST;
-                    mbar_wait_lazy(&s.empty_k[sk], ((g / KST) & 1) ^ 1);
+                    mbar_wait_sleep(&s.empty_k[sk], ((g / KST) & 1) ^ 1);
                     mbar_arrive_tx(&s.full_k[sk], kbytes);
                     uint8_t *stg = s.buf + sk * Ring<MODE>::stage;
                     tma_load_2d(stg, &tmK, &s.full_k[sk], kb * BK, tile * BM, pol_stream);
@@ -223,7 +231,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nkb; kb++, g++) {
                     const int sq = g % QST;
-                    mbar_wait_lazy(&s.empty_q[sq], ((g / QST) & 1) ^ 1);
+                    mbar_wait_sleep(&s.empty_q[sq], ((g / QST) & 1) ^ 1);
                     mbar_arrive_tx(&s.full_q[sq], 2 * QTILE);
                     bulk_load(s.q[sq], p.qsplit + (size_t)kb * (2 * BN * BK), 2 * QTILE, &s.full_q[sq], pol_keep);
                 }
@@ -241,7 +249,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nkb; kb++, g++) {
                     const int sk = g % KST;
-                    mbar_wait_lazy(&s.staged[sk], (g / KST) & 1);
+                    mbar_wait_sleep(&s.staged[sk], (g / KST) & 1);
                     tma_store_2d(&tmKh, s.buf + sk * Ring<MODE>::stage, kb * BK, tile * BM, pol_out);
                     const bool group_end = (kb % CODE_KB) == CODE_KB - 1 || kb == nkb - 1;
                     if (group_end)
@@ -268,12 +276,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const bool chunk_first = (kb % CHUNK_KB) == 0;
                     const bool chunk_last = (kb % CHUNK_KB) == CHUNK_KB - 1 || kb == nkb - 1;
                     if (chunk_first) {
-                        mbar_wait(&s.empty_acc[ab], ((gc >> 1) & 1) ^ 1);
+                        KVQ_WAIT_HOT(&s.empty_acc[ab], ((gc >> 1) & 1) ^ 1);
                         tc_fence_after();
                     }
                     const int sa = g % AST, sq = g % QST;
-                    mbar_wait(&s.full_a[sa], (g / AST) & 1);
-                    mbar_wait(&s.full_q[sq], (g / QST) & 1);
+                    KVQ_WAIT_HOT(&s.full_a[sa], (g / AST) & 1);
+                    KVQ_WAIT_HOT(&s.full_q[sq], (g / QST) & 1);
                     tc_fence_after();
                     const uint32_t ahi = tbase + A_COL0 + sa * 64, alo = ahi + 32;
                     const uint32_t qhi = smem_u32(s.q[sq]), qlo = qhi + QTILE;
@@ -308,7 +316,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             for (int kb = 0; kb < nkb; kb++, g++) {
                 const int sk = g % KST;
-                mbar_wait(&s.full_k[sk], (g / KST) & 1);
+                KVQ_WAIT_HOT(&s.full_k[sk], (g / KST) & 1);
                 const uint32_t kbase = smem_u32(s.buf + sk * Ring<MODE>::stage);
                 float e[16];
                 if (MODE != 2) {
@@ -370,7 +378,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     // K_hat overwrites x in the input stage (same swizzled positions, read by this
                     // thread only); the codes go to the group's code buffer.  The store warp writes
                     // both out with TMA and then frees the stage (and the code buffer).
-                    if ((kb % CODE_KB) == 0) mbar_wait(&s.cstored[cgrp & 1], ((cgrp >> 1) & 1) ^ 1);
+                    if ((kb % CODE_KB) == 0) KVQ_WAIT_HOT(&s.cstored[cgrp & 1], ((cgrp >> 1) & 1) ^ 1);
                     const uint32_t cds = smem_u32(s.buf + 128 * 1024 + (cgrp & 1) * KTILE);
 #pragma unroll
                     for (int c = 0; c < 4; c++)
@@ -407,7 +415,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     lo[i] = __float_as_uint(__fsub_rn(e[i], __uint_as_float(hi[i])));
                 }
                 const int sa = g % AST;
-                mbar_wait(&s.empty_a[sa], ((g / AST) & 1) ^ 1);
+                KVQ_WAIT_HOT(&s.empty_a[sa], ((g / AST) & 1) ^ 1);
                 tc_fence_after();
                 tmem_st16(tbase + lane_off + A_COL0 + sa * 64 + 16 * h, hi);
                 tmem_st16(tbase + lane_off + A_COL0 + sa * 64 + 32 + 16 * h, lo);
@@ -442,7 +450,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int j = 0; j < BN; j++) acc[j] = 0.0;
             for (int c = 0; c < nchunks; c++, gc++) {
                 const int ab = gc & 1;
-                mbar_wait_lazy(&s.full_acc[ab], (gc >> 1) & 1);
+                mbar_wait_sleep(&s.full_acc[ab], (gc >> 1) & 1);
                 tc_fence_after();
                 uint32_t v[32];
 #pragma unroll

@@ -9,11 +9,12 @@
 //   fq = RN(x * y);  c = clamp(fq, +-127);  v = RN(c + 1.5*2^23)   (half-even rint)
 //   q  = low byte of bits(v);  r = v - 1.5*2^23  (= (float)q exactly)
 // Error bound (s normal, |x/s| <= 128): y = (1/s)(1+d1), fq = x*y*(1+d2),
-// |d1|,|d2| <= 2^-24  =>  |fq - x/s| <= 2^-16 and |RN(x/s) - x/s| <= 2^-18, so
-// |fq - RN(x/s)| < 2^-15.  Whenever c is farther than 2^-12 from every half
-// integer, fq and the exact quotient RN(x/s) lie strictly inside the same
-// rounding interval and give the same code.  Otherwise ("danger", probability
-// ~1e-4 per element) the element is recomputed with the IEEE division
+// |d1|,|d2| <= 2^-24  =>  |fq - x/s| <= 128 * 2^-23 = 2^-16 and
+// |RN(x/s) - x/s| <= 2^-18, so |fq - RN(x/s)| < 2^-15.  Whenever c is farther
+// than 2^-14 (a 2x margin) from every half integer, fq and the exact quotient
+// RN(x/s) lie strictly inside the same rounding interval and give the same
+// code.  Otherwise ("danger", probability 2^-13 per element for uniform
+// quotients) the element is recomputed with the IEEE division
 // __fdiv_rn, which decides ties exactly as the oracle.  Quotients beyond
 // +-127.5 clamp identically on both sides.  Subnormal scales (s < 2^-126,
 // where RN(1/s) may overflow) take the exact path for the whole column.
@@ -25,7 +26,7 @@
 namespace kvq {
 
 constexpr float kMagic = 12582912.0f;          // 1.5 * 2^23: RN(c + kMagic) - kMagic == rint(c), |c| < 2^22
-constexpr float kDangerThr = 0.5f - 0x1p-12f;  // distance to nearest integer above which we re-check
+constexpr float kDangerThr = 0.5f - 0x1p-14f;  // distance to nearest integer above which we re-check
 constexpr float kMinNormal = 1.17549435e-38f;  // 2^-126
 
 struct ColQ {

@@ -8,7 +8,7 @@
 // (per = 8 / bits, low bits first); unused bits are 0.
 //
 // Same column-owning streaming geometry and the same provably-exact division
-// as the INT8 kernels (device_common.cuh: RN(1/s) hoisted per column, a 2^-12
+// as the INT8 kernels (device_common.cuh: RN(1/s) hoisted per column, a 2^-14
 // danger band around half-integers recomputed with the IEEE quotient; the bound
 // needs |x/s| <= 128, far above qmax).  The magic-constant rint leaves the code's
 // two's complement in the low bits of the float, so a word of packed codes is

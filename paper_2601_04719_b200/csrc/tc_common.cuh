@@ -42,6 +42,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
     while (!mbar_try_wait(a, parity)) {
     }
 }
+// Suspend in hardware until the phase completes (or `ns` elapse): no spin loop
+// issuing instructions (and burning power) while a role waits.
+__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t addr, uint32_t parity, uint32_t ns) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity), "r"(ns)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *b, uint32_t parity) {
+    const uint32_t a = smem_u32(b);
+    while (!mbar_try_wait_hint(a, parity, 1000000u)) {
+    }
+}
 // For roles that mostly wait (epilogue, store warp, producers): back off between
 // polls so idle warps do not burn issue slots and power under the 1 kW cap.
 __device__ __forceinline__ void mbar_wait_lazy(uint64_t *b, uint32_t parity) {
