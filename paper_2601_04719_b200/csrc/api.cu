@@ -328,8 +328,7 @@ extern "C" kvq_status kvq_error_metrics_async(const float *K, const float *K_hat
     KVQ_TRY(launch_metrics_partials(K, K_hat, T, D, nq ? Q : nullptr, nq, scales, workspace, workspace_bytes, &tot,
                                     s));
     if (comm) {
-        KVQ_TRY(comm_allreduce_sum_f64(comm, tot.sums, 4, s));
-        KVQ_TRY(comm_allreduce_max_u64(comm, tot.maxes, 2, s));
+        KVQ_TRY(comm_allreduce_metrics(comm, tot.sums, 4, tot.maxes, 2, s));
     }
     return launch_metrics_finalize(tot, out_dev, s);
 }
@@ -372,8 +371,7 @@ extern "C" kvq_status kvq_roundtrip(const float *K, const float *scales, int64_t
     KVQ_TRY(launch_roundtrip_partials(K, scales, T, D, Kq, K_hat, nq ? Q : nullptr, nq, workspace, workspace_bytes,
                                       &tot, s));
     if (comm) {
-        KVQ_TRY(comm_allreduce_sum_f64(comm, tot.sums, 4, s));
-        KVQ_TRY(comm_allreduce_max_u64(comm, tot.maxes, 2, s));
+        KVQ_TRY(comm_allreduce_metrics(comm, tot.sums, 4, tot.maxes, 2, s));
     }
     return launch_metrics_finalize(tot, out_dev, s);
 }
@@ -506,8 +504,7 @@ static kvq_status roundtrip_host_enqueue(const float *K_host, int64_t T, int64_t
                                             metrics_workspace_size(T, D, nq), &tot, s)) != KVQ_OK)
             break;
         if (comm) {
-            if ((st = comm_allreduce_sum_f64(comm, tot.sums, 4, s)) != KVQ_OK) break;
-            if ((st = comm_allreduce_max_u64(comm, tot.maxes, 2, s)) != KVQ_OK) break;
+            if ((st = comm_allreduce_metrics(comm, tot.sums, 4, tot.maxes, 2, s)) != KVQ_OK) break;
         }
         if ((st = launch_metrics_finalize(tot, mout, s)) != KVQ_OK) break;
         // results back on the D2H copy engine

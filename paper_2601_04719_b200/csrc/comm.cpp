@@ -35,6 +35,8 @@ struct NcclApi {
     ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     const char *(*getErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
 };
 
 NcclApi &api() {
@@ -58,7 +60,10 @@ NcclApi &api() {
         a.commDestroy = (decltype(a.commDestroy))dlsym(h, "ncclCommDestroy");
         a.allReduce = (decltype(a.allReduce))dlsym(h, "ncclAllReduce");
         a.getErrorString = (decltype(a.getErrorString))dlsym(h, "ncclGetErrorString");
-        a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.allReduce && a.getErrorString;
+        a.groupStart = (decltype(a.groupStart))dlsym(h, "ncclGroupStart");
+        a.groupEnd = (decltype(a.groupEnd))dlsym(h, "ncclGroupEnd");
+        a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.allReduce && a.getErrorString &&
+               a.groupStart && a.groupEnd;
         if (!a.ok) a.err = "NCCL library lacks required symbols";
     });
     return a;
@@ -88,6 +93,21 @@ kvq_status comm_allreduce_sum_f64(kvq_comm_t comm, double *buf, size_t count, cu
 }
 kvq_status comm_allreduce_max_u64(kvq_comm_t comm, uint64_t *buf, size_t count, cudaStream_t s) {
     return allreduce(comm, buf, count, ncclUint64, ncclMax, s, "allreduce(max,u64)");
+}
+// The metric partials (a5/a6): fp64 sums (SUM) and u64 bit-pattern maxima (MAX)
+// in ONE NCCL group, i.e. one fused launch instead of two per step.
+kvq_status comm_allreduce_metrics(kvq_comm_t comm, double *sums, size_t nsum, uint64_t *maxes, size_t nmax,
+                                  cudaStream_t s) {
+    NcclApi &a = api();
+    if (!a.ok) return fail(KVQ_ERR_NCCL, a.err);
+    ncclResult_t r = a.groupStart();
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
+    kvq_status st = allreduce(comm, sums, nsum, ncclFloat64, ncclSum, s, "allreduce(sum,f64)");
+    if (st == KVQ_OK) st = allreduce(comm, maxes, nmax, ncclUint64, ncclMax, s, "allreduce(max,u64)");
+    r = a.groupEnd();
+    if (st != KVQ_OK) return st;
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGroupEnd");
+    return KVQ_OK;
 }
 
 }  // namespace kvq

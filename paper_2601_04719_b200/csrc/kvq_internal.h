@@ -106,5 +106,7 @@ kvq_status launch_scores_codes(const float *Q, int64_t nq, const int8_t *Kq, con
 kvq_status comm_allreduce_max_u32(kvq_comm_t comm, uint32_t *buf, size_t count, cudaStream_t s);
 kvq_status comm_allreduce_sum_f64(kvq_comm_t comm, double *buf, size_t count, cudaStream_t s);
 kvq_status comm_allreduce_max_u64(kvq_comm_t comm, uint64_t *buf, size_t count, cudaStream_t s);
+kvq_status comm_allreduce_metrics(kvq_comm_t comm, double *sums, size_t nsum, uint64_t *maxes, size_t nmax,
+                                  cudaStream_t s);
 
 }  // namespace kvq
