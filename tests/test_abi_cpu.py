@@ -102,3 +102,28 @@ def test_binding_import_and_errors():
         kvq.kvq_compute_scales(torch.zeros(4, 4))  # CPU tensor: no CPU path
     with pytest.raises(TypeError):
         kvq.kvq_quantize(torch.zeros(4, 4, dtype=torch.float64), torch.zeros(4))
+
+
+def test_next_rows_validation_without_gpu(lib):
+    """FP8 / INT4-INT2 / scores-from-codes / append entry points validate their
+    arguments synchronously and fail loudly (no CPU path) when they are valid."""
+    import torch
+    from paper_2601_04719_b200._lib import ERR_INVALID_VALUE, OK
+    A = 1 << 20
+    assert lib.kvq_compute_scales_fmt(A, 4, 4, 2 * A, 9, None, None) == ERR_INVALID_VALUE  # unknown format
+    assert lib.kvq_packed_row_bytes(9, 4) == 5 and lib.kvq_packed_row_bytes(9, 2) == 3
+    assert lib.kvq_packed_row_bytes(9, 3) == -1 and lib.kvq_packed_row_bytes(0, 4) == -1
+    assert lib.kvq_quantize_packed(A, 2 * A, 4, 8, 3, 3 * A, None, None) == ERR_INVALID_VALUE  # bits
+    assert lib.kvq_quantize_packed(A, 2 * A, 4, 8, 4, A + 4, None, None) == ERR_INVALID_VALUE  # Kp aliases K
+    assert lib.kvq_dequantize_packed(A, 2 * A, 4, 8, 2, A, None) == ERR_INVALID_VALUE  # K_hat aliases Kp
+    assert lib.kvq_quantize_e4m3(A, 2 * A, 4, 4, A + 2, None, None) == ERR_INVALID_VALUE
+    assert lib.kvq_append_workspace_size(8) >= 8 * 4 and lib.kvq_append_workspace_size(0) == 0
+    ws = lib.kvq_append_workspace_size(8)
+    assert lib.kvq_append(A, -1, 1, 8, 2 * A, 3 * A, 4 * A, None, 5 * A, ws, None, None) == ERR_INVALID_VALUE
+    assert lib.kvq_append(A, 0, 1, 8, 2 * A, 3 * A, 4 * A, None, 5 * A, 1, None, None) == ERR_INVALID_VALUE  # ws
+    assert lib.kvq_append(A, 0, 4, 8, A + 8, 3 * A, 4 * A, None, 5 * A, ws, None, None) == ERR_INVALID_VALUE  # alias
+    assert lib.kvq_scores_from_codes_workspace_size(1024, 64) > 0
+    if not torch.cuda.is_available():
+        assert lib.kvq_quantize_packed(A, 2 * A, 4, 8, 4, 3 * A, None, None) != OK
+        assert lib.kvq_append(A, 0, 1, 8, 2 * A, 3 * A, 4 * A, None, 5 * A, ws, None, None) != OK
+        assert lib.kvq_scores_from_codes(A, 4, 2 * A, 3 * A, 8, 16, 4 * A, None, 0, None) != OK
