@@ -66,7 +66,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for s in SOURCES:
         o = os.path.join(objdir, s.rsplit(".", 1)[0] + ".o")
-        cmd = [nvcc(), *ARCH, *NVFLAGS, *inc, "-c", os.path.join(CSRC, s), "-o", o]
+        extra = os.environ.get("KVQ_NVCC_EXTRA", "").split()  # experiments only (e.g. -DKVQ_SPIN_ALL)
+        cmd = [nvcc(), *ARCH, *NVFLAGS, *extra, *inc, "-c", os.path.join(CSRC, s), "-o", o]
         if verbose and s.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]
         if verbose:

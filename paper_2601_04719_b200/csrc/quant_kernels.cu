@@ -233,6 +233,106 @@ __global__ void __launch_bounds__(kThreads) dequant_v4_kernel(const uint32_t *__
     }
 }
 
+// ============================================================================ row-slab grid variants
+// The same element arithmetic as quant_v4_kernel / dequant_v4_kernel on a
+// non-persistent grid: block b covers a slab of kSlabU x RS rows by CW float4
+// columns (CW = min(D/4, 256), RS = 256 / CW) and retires.  Consecutive blocks
+// take the adjacent column chunks of the same rows, so the hardware block
+// scheduler walks K in address order and the DRAM pages written at any moment
+// form one narrow moving window.  Measured on B200 at C4
+// (scripts/probes/bw_mix2.cu, profiles/r01/hbm_patterns.md): such grids reach
+// 6.9 TB/s on the quantize+dequantize traffic mix where persistent grid-stride
+// loops (whose blocks drift apart and widen the window) reach 5.6 TB/s -- for
+// write-heavy traffic the width of the window sets the bandwidth.  Each thread
+// keeps the column-owning idea inside its slab: one float4 of columns, its
+// scales and RN(1/s) formed once and reused for kSlabU rows.
+constexpr int kSlabU = 4;
+
+struct SlabGeom {
+    uint32_t cols4, CW, RS, NCC;  // float4 columns, chunk width, rows per slice, chunks per row
+    int64_t T;
+};
+
+static SlabGeom slab_geom(int64_t T, int64_t cols4) {
+    SlabGeom g;
+    g.cols4 = (uint32_t)cols4;
+    g.CW = (uint32_t)std::min<int64_t>(cols4, kThreads);
+    g.RS = kThreads / g.CW;
+    g.NCC = (uint32_t)((cols4 + g.CW - 1) / g.CW);
+    g.T = T;
+    return g;
+}
+static int64_t slab_blocks(const SlabGeom &g) {
+    return (int64_t)g.NCC * ((g.T + (int64_t)g.RS * kSlabU - 1) / ((int64_t)g.RS * kSlabU));
+}
+
+// thread -> (first row, float4 column); false if the thread has no column
+__device__ __forceinline__ bool slab_coords(const SlabGeom &g, int64_t &row0, uint32_t &c) {
+    const uint32_t rs = threadIdx.x / g.CW, cl = threadIdx.x - rs * g.CW;
+    const uint32_t cc = blockIdx.x % g.NCC;
+    c = cc * g.CW + cl;
+    row0 = (int64_t)(blockIdx.x / g.NCC) * (g.RS * kSlabU) + rs;
+    return rs < g.RS && c < g.cols4;
+}
+
+template <int SP = 1>
+__global__ void __launch_bounds__(kThreads) dequant_slab_kernel(const uint32_t *__restrict__ Kq4,
+                                                                const float4 *__restrict__ scales4,
+                                                                float4 *__restrict__ Kh4, const SlabGeom g) {
+    int64_t row0;
+    uint32_t c;
+    if (!slab_coords(g, row0, c)) return;
+    uint32_t w[kSlabU];
+#pragma unroll
+    for (int k = 0; k < kSlabU; k++) {
+        const int64_t row = row0 + (int64_t)k * g.RS;
+        if (row < g.T) w[k] = ld_stream_u32(Kq4 + row * g.cols4 + c);
+    }
+    const float4 s = __ldg(scales4 + c);
+#pragma unroll
+    for (int k = 0; k < kSlabU; k++) {
+        const int64_t row = row0 + (int64_t)k * g.RS;
+        if (row < g.T) {
+            float4 o;
+            o.x = __fmul_rn(code_to_float(w[k], 0), s.x);
+            o.y = __fmul_rn(code_to_float(w[k], 1), s.y);
+            o.z = __fmul_rn(code_to_float(w[k], 2), s.z);
+            o.w = __fmul_rn(code_to_float(w[k], 3), s.w);
+            store_f4<SP>(Kh4 + row * g.cols4 + c, o);
+        }
+    }
+}
+
+template <bool FUSED, int SP = 1>
+__global__ void __launch_bounds__(kThreads) quant_slab_kernel(const float4 *__restrict__ K,
+                                                              const float4 *__restrict__ scales4,
+                                                              uint32_t *__restrict__ Kq4, float4 *__restrict__ Kh4,
+                                                              const SlabGeom g) {
+    int64_t row0;
+    uint32_t c;
+    if (!slab_coords(g, row0, c)) return;
+    float4 v[kSlabU];
+#pragma unroll
+    for (int k = 0; k < kSlabU; k++) {
+        const int64_t row = row0 + (int64_t)k * g.RS;
+        if (row < g.T) v[k] = ld_stream_f4(K + row * g.cols4 + c);
+    }
+    const float4 s = __ldg(scales4 + c);
+    const ColQ q0 = make_colq(s.x), q1 = make_colq(s.y), q2 = make_colq(s.z), q3 = make_colq(s.w);
+    const bool col_exact = q0.exact | q1.exact | q2.exact | q3.exact;
+#pragma unroll
+    for (int k = 0; k < kSlabU; k++) {
+        const int64_t row = row0 + (int64_t)k * g.RS;
+        if (row < g.T) {
+            uint32_t w;
+            float4 xh;
+            quant4<FUSED>(v[k], q0, q1, q2, q3, col_exact, w, xh);
+            store_u32<SP>(Kq4 + row * g.cols4 + c, w);
+            if (FUSED) store_f4<SP>(Kh4 + row * g.cols4 + c, xh);
+        }
+    }
+}
+
 template <int U>
 __global__ void __launch_bounds__(kThreads) dequant_scalar_kernel(const int8_t *__restrict__ Kq,
                                                                   const float *__restrict__ scales,
@@ -371,6 +471,11 @@ StreamPlan plan_stream(int64_t rows, int64_t cols, int threads_per_sm) {
 
 constexpr int kUColmax = 8, kUQuant = 4, kUDequant = 8;
 
+// Row-slab kernels: scales read as float4 (16-byte aligned), grid.x < 2^31, cols4 < 2^31.
+static bool slab_ok(int64_t cols4, const float *scales) {
+    return aligned(scales, 16) && cols4 < (1LL << 31);
+}
+
 // Resident threads per SM for `kernel` at kThreads per CTA: the grid is sized
 // to exactly one full wave of resident threads (no tail wave).
 template <typename Kern>
@@ -421,7 +526,14 @@ kvq_status launch_quantize(const float *K, const float *scales, int64_t T, int64
         auto K4 = reinterpret_cast<const float4 *>(K);
         auto Q4 = reinterpret_cast<uint32_t *>(Kq);
         auto H4 = reinterpret_cast<float4 *>(K_hat);
-        if (K_hat) {
+        const SlabGeom sg = slab_geom(T, cols4);
+        // quantize + dequantize (R4 W5, write-heavy): row-slab grid, 1.40 vs 1.75 ms at C4.
+        // quantize alone (R4 W1, read-heavy): the persistent column-owning kernel stays ahead
+        // (0.86 vs 0.92 ms at C4, same box), so it keeps the grid-stride geometry.
+        if (K_hat && slab_ok(cols4, scales) && slab_blocks(sg) < (1LL << 31)) {
+            quant_slab_kernel<true><<<(unsigned)slab_blocks(sg), kThreads, 0, s>>>(
+                K4, reinterpret_cast<const float4 *>(scales), Q4, H4, sg);
+        } else if (K_hat) {
             StreamPlan p = plan_stream(T, cols4, KVQ_RESIDENT((quant_v4_kernel<kUQuant, true, 1>), 0));
             quant_v4_kernel<kUQuant, true, 1><<<p.blocks, kThreads, 0, s>>>(K4, scales, Q4, H4, n / 4, cols4, p.G);
         } else {
@@ -442,7 +554,13 @@ kvq_status launch_quantize(const float *K, const float *scales, int64_t T, int64
 kvq_status launch_dequantize(const int8_t *Kq, const float *scales, int64_t T, int64_t D, float *K_hat,
                              cudaStream_t s) {
     const int64_t n = T * D;
-    if (D % 4 == 0 && aligned(Kq, 4) && aligned(K_hat, 16)) {
+    if (D % 4 == 0 && aligned(Kq, 4) && aligned(K_hat, 16) && slab_ok(D / 4, scales) &&
+        slab_blocks(slab_geom(T, D / 4)) < (1LL << 31)) {
+        const SlabGeom sg = slab_geom(T, D / 4);
+        dequant_slab_kernel<<<(unsigned)slab_blocks(sg), kThreads, 0, s>>>(reinterpret_cast<const uint32_t *>(Kq),
+                                                                          reinterpret_cast<const float4 *>(scales),
+                                                                          reinterpret_cast<float4 *>(K_hat), sg);
+    } else if (D % 4 == 0 && aligned(Kq, 4) && aligned(K_hat, 16)) {
         const int64_t cols4 = D / 4;
         StreamPlan p = plan_stream(T, cols4, KVQ_RESIDENT((dequant_v4_kernel<kUDequant, 1>), 0));
         dequant_v4_kernel<kUDequant, 1><<<p.blocks, kThreads, 0, s>>>(
