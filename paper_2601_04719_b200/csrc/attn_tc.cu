@@ -11,29 +11,22 @@
 // One persistent CTA per SM walks 128-row tiles; per 32-column K-block:
 //   warp 0 (1 lane)  TMA: K (and K_hat) boxes [128 x 32] fp32 (128B swizzle) and,
 //                    in the fused mode, the 32 per-column quantizer constants into
-//                    an 8-stage (fused) / 4-stage ring.
-//   warp 3 (1 lane)  1-D bulk copy of the pre-split Q tile ([Q_hi; Q_lo] as one
-//                    128-row tf32 tile, 16 KB, already in the canonical UMMA layout)
-//                    into a 4-stage ring that advances with the A ring.
-//   warps 4..19      16 converter warps, one token row and 8 columns per thread
-//                    (ld.shared): [fused mode: quantize (Eq. 7) + dequantize (Eq. 8)
-//                    the row segment, write K_hat in place into the input stage and
-//                    the codes into a [128 x 128 B] staging buffer];
+//                    a 4-stage ring; 1-D bulk copy of the pre-split Q tile (hi+lo,
+//                    16 KB, already in the canonical UMMA layout) into a 4-stage ring.
+//   warps 4..11      converters, one token row and 16 columns per thread (ld.shared):
+//                    [fused mode: quantize (Eq. 7) + dequantize (Eq. 8) the row
+//                    segment, stage codes and K_hat in swizzled smem and write them
+//                    with TMA bulk tensor stores (full 128-byte lines: no DRAM
+//                    read-modify-write for the 32-byte code segments)]
 //                    E = K - K_hat, sum E^2 and max |E| (a5), split E into tf32
-//                    hi/lo and tcgen05.st them into a 4-stage A ring in TMEM (the A
-//                    operand is read from TMEM: no smem bandwidth for E's reads).
-//   warp 2 (1 lane)  [fused mode] TMA bulk-tensor stores of the K_hat box and, every
-//                    4 K-blocks, of the code box (full 128-byte lines: no DRAM
-//                    read-modify-write); frees the input stage one block later.
-//   warp 1           MMA issuer: the whole warp runs the loop (descriptors stay in
-//                    uniform registers), one elected lane issues per K-step
-//                    E_hi x [Q_hi; Q_lo] (M=128, N=128, K=8) and E_lo x Q_hi (N=64)
-//                    into a double-buffered TMEM accumulator, restarted every
-//                    CHUNK_KB K-blocks; one commit per K-block frees the A and Q stages.
-//   warps 20..23     epilogue (registers raised with setmaxnreg), one row per thread:
-//                    tcgen05.ld each finished [128 x 128] fp32 chunk accumulator and
-//                    add both halves into fp64 registers; at the end of a tile sum
-//                    |Delta| (fp64) or store S.
+//                    hi/lo and tcgen05.st them into a 2-stage A ring in TMEM (the A
+//                    operand is read from TMEM: no smem bandwidth for E's 3 reads).
+//   warp 1 (1 lane)  issues 3 x 4 tcgen05.mma (M=128, N=64, K=8) per K-block into a
+//                    double-buffered TMEM accumulator, restarted every CHUNK_KB
+//                    K-blocks, and commits to the barriers.
+//   warps 12..15     epilogue (registers raised with setmaxnreg), one row per thread: tcgen05.ld each finished
+//                    [128 x 64] fp32 chunk accumulator and add it into fp64
+//                    registers; at the end of a tile sum |Delta| (fp64) or store S.
 // The tensor core's fp32 accumulation is not round-to-nearest: accumulating all
 // D/8 * 3 MMA steps of D = 8192 in TMEM biased |Delta| by ~5e-5 (measured on
 // B200).  Restarting the accumulator every 128 columns (48 MMA steps) and
@@ -52,8 +45,6 @@ namespace kvq {
 namespace tc {
 
 constexpr int BM = 128, BN = 64, BK = 32;
-// Q ring and A ring have the same depth and advance together: one tcgen05.commit per K-block
-// (empty_a) releases both stages.
 constexpr int QST = 4, AST = 4;
 // Input ring: modes 0/1 stage K and K_hat (32 KB) x 4; the fused mode stages K only
 // (16 KB) x 8, i.e. 128 KB in flight per SM either way (Little's law at ~44 GB/s/SM).
@@ -63,38 +54,19 @@ struct Ring {
     static constexpr int kst = MODE == 2 ? 8 : 4;
     static constexpr uint32_t stage = MODE == 2 ? 16384u : 32768u;
 };
-// warps: 0 K producer, 1 MMA (+TMEM alloc), 2 code stores (fused mode), 3 Q producer, 4..4+NCONV_W-1
-// converters (NCONV_W/4 per TMEM lane quarter, CPT columns of each 32-column K-block each), then 4
-// epilogue warps.  Warpgroup 0 and the converters give registers to the epilogue warpgroup
-// (setmaxnreg), which keeps 64 fp64 accumulators per row.  16 converter warps (4 per SM sub-partition)
-// hide the latency of the per-element dependency chain (smem load -> quantize -> E -> split -> TMEM
-// store) that 8 warps left exposed (the converters were the roundtrip's bottleneck once its HBM
-// traffic shrank to 4 + 1 B/elem).
-constexpr int NCONV_W = 16;
-constexpr int CPT = BK * 4 / NCONV_W;  // columns per converter thread per K-block (8)
-constexpr int NTHREADS = 32 * (4 + NCONV_W + 4);
-constexpr int NCONV = 32 * NCONV_W;  // converter threads
-constexpr int CONV_W0 = 4, EPI_W0 = 4 + NCONV_W;
-// register split (65536 per SM, one CTA): warpgroup 0, converters, epilogue
-constexpr uint32_t REG_WG0 = 40, REG_CONV = 64, REG_EPI = 184;
-static_assert(128 * REG_WG0 + NCONV * REG_CONV + 128 * REG_EPI <= 65536, "register budget");
-static_assert(CPT == 8, "converter width");
+// warps: 0 K producer, 1 MMA (+TMEM alloc), 2 output stores (fused mode), 3 Q producer, 4-11 converters (2 per TMEM lane
+// quarter, 16 columns each), 12-15 epilogue.  Warpgroup 0 gives registers to the
+// epilogue warpgroup (setmaxnreg), which keeps 64 fp64 accumulators per row.
+constexpr int NTHREADS = 512;
+constexpr int NCONV = 256;  // converter threads
+constexpr int CONV_W0 = 4, EPI_W0 = 12;
 constexpr int CHUNK_KB = 4;              // K-blocks (of 32 columns) per TMEM accumulation chunk
 constexpr int CODE_KB = 4;               // K-blocks per code store (128 codes = one 128 B line per row)
 constexpr uint32_t KTILE = BM * BK * 4;  // 16 KB
 constexpr uint32_t QTILE = BN * BK * 4;  // 8 KB (one of hi/lo)
-constexpr uint32_t TMEM_COLS = 512;      // acc 2 x 128 (N = 2 x 64: E_hi.Q_hi | E_hi.Q_lo) | A ring 4 x (hi 32 + lo 32)
-constexpr uint32_t ACC_COLS = 2 * BN;    // one accumulator buffer
-constexpr uint32_t A_COL0 = 2 * ACC_COLS;
-static_assert(A_COL0 + AST * 64 <= TMEM_COLS, "TMEM budget");
-constexpr uint32_t IDESC = idesc_tf32(BM, BN);        // E_lo x Q_hi       (N = 64)
-constexpr uint32_t IDESC2 = idesc_tf32(BM, 2 * BN);   // E_hi x [Q_hi; Q_lo] (N = 128)
-
-// K-blocks per tile row: ceil(D / BK) rounded up to a multiple of CODE_KB.  The padding K-blocks
-// lie wholly past column D: TMA fills their K boxes with zeros and clips their code stores, their
-// Q tiles and column records are zero (code 0, E = 0), so they add nothing -- and every code group
-// and accumulator chunk is complete, which the two converter groups rely on.
-static inline int64_t nkb_of(int64_t D) { return ((D + BK - 1) / BK + CODE_KB - 1) / CODE_KB * CODE_KB; }
+constexpr uint32_t TMEM_COLS = 512;      // acc 2 x 64 | A ring AST x (hi 32 + lo 32) (| 128 spare)
+constexpr uint32_t A_COL0 = 128;
+constexpr uint32_t IDESC = idesc_tf32(BM, BN);
 
 // Per K-block quantizer record (fused mode): {s, RN(1/s)} of the 32 columns and a
 // flag set when one of them needs the exact path for every element.
@@ -111,18 +83,6 @@ struct __align__(16) ColRec {
 #else
 #define KVQ_WAIT_HOT mbar_wait
 #endif
-// Converter waits: suspend in try_wait (no issue slots taken from the MMA issuer, which shares
-// its SM sub-partition with 4 converter warps) unless overridden (experiments).
-#ifndef KVQ_WAIT_CONV
-#define KVQ_WAIT_CONV mbar_wait_sleep
-#endif
-// Waits of the roles that mostly idle (producers, store warp, epilogue): suspend in
-// try_wait, or spin when built with -DKVQ_SPIN_ALL (experiments).
-#ifdef KVQ_SPIN_ALL
-#define KVQ_WAIT_COLD mbar_wait
-#else
-#define KVQ_WAIT_COLD mbar_wait_sleep
-#endif
 
 struct __align__(1024) Smem {
     // modes 0/1: stage i = [K box | K_hat box] at 32 KB * i (4 stages)
@@ -132,11 +92,11 @@ struct __align__(1024) Smem {
     uint8_t buf[160 * 1024];
     uint8_t q[QST][2 * QTILE];
     ColRec cq[KST_MAX];      // fused mode: per-column quantizer constants of the K-block
-    uint64_t full_k[KST_MAX], empty_k[KST_MAX], full_q[QST];
+    uint64_t full_k[KST_MAX], empty_k[KST_MAX], full_q[QST], empty_q[QST];
     uint64_t full_a[AST], empty_a[AST], full_acc[2], empty_acc[2];
     uint64_t staged[KST_MAX], cstored[2];  // fused mode: handoff converters -> store warp -> converters
     uint32_t tmem_base;
-    double red[3][NCONV_W];
+    double red[3][8];
 };
 
 static_assert(sizeof(Smem) <= 227 * 1024, "shared memory budget (227 KB per CTA on sm_100)");
@@ -153,12 +113,10 @@ struct TcParams {
     float *Kh;           // MODE 2: K_hat output [T][D]
 };
 
-// Q [nq][D] -> per K-block kb: one [2*BN x BK] tf32 tile, rows 0..63 = Q_hi, rows
-// 64..127 = Q_lo, in the canonical K-major SWIZZLE_NONE layout: core matrix
-// (kg = k/4, rg = n/8) at byte (kg*16 + rg)*128, row n%8 at +16*(n%8), element k%4
-// at +4*(k%4) (LBO = 2048 between k-groups, SBO = 128 between row groups).  One
-// N = 128 MMA reads both halves (E_hi x [Q_hi; Q_lo]); an N = 64 MMA on the same
-// descriptor reads the Q_hi half only.  Rows >= nq and columns >= D are zero.
+// Q [nq][D] -> per K-block kb: [hi | lo] tiles of BN x BK tf32 in the canonical
+// K-major SWIZZLE_NONE layout: core matrix (kg = k/4, rg = n/8) at byte
+// (kg*8 + rg)*128, row n%8 at +16*(n%8), element k%4 at +4*(k%4).  Rows >= nq
+// and columns >= D are zero.
 __global__ void qsplit_kernel(const float *__restrict__ Q, int64_t nq, int64_t D, int64_t nkb,
                               uint32_t *__restrict__ out) {
     const int64_t total = nkb * BN * BK;
@@ -170,10 +128,10 @@ __global__ void qsplit_kernel(const float *__restrict__ Q, int64_t nq, int64_t D
         const float q = (n < nq && col < D) ? Q[n * D + col] : 0.0f;
         const uint32_t hi = to_tf32(q);
         const uint32_t lo = to_tf32(q - __uint_as_float(hi));
-        const uint32_t off = ((k / 4) * 16 + n / 8) * 32 + (n % 8) * 4 + (k % 4);  // in 4-byte words
+        const uint32_t off = ((k / 4) * 8 + n / 8) * 32 + (n % 8) * 4 + (k % 4);  // in 4-byte words
         uint32_t *tile = out + kb * (2 * BN * BK);
         tile[off] = hi;
-        tile[off + (BN / 8) * 32] = lo;  // row n + 64
+        tile[BN * BK + off] = lo;
     }
 }
 
@@ -222,6 +180,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         for (int i = 0; i < QST; i++) {
             mbar_init(&s.full_q[i], 1);
+            mbar_init(&s.empty_q[i], 1);
         }
         for (int i = 0; i < AST; i++) {
             mbar_init(&s.full_a[i], NCONV);
@@ -246,7 +205,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t tbase = s.tmem_base;
 
     if (warp < CONV_W0) {
-        setmaxnreg_dec<REG_WG0>();  // warpgroup 0: producers, MMA issuer, store warp need few registers
+        setmaxnreg_dec<56>();  // warpgroup 0: producer + MMA issuer need few registers
         if (warp == 0 && lane == 0) {
             // ------------------------------------------------------------ producer
             const uint64_t pol_stream = (p.hints & 1) ? policy_evict_first() : policy_evict_normal();
@@ -256,7 +215,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nkb; kb++, g++) {
                     const int sk = g % KST;
-                    KVQ_WAIT_COLD(&s.empty_k[sk], ((g / KST) & 1) ^ 1);
+                    mbar_wait_sleep(&s.empty_k[sk], ((g / KST) & 1) ^ 1);
                     mbar_arrive_tx(&s.full_k[sk], kbytes);
                     uint8_t *stg = s.buf + sk * Ring<MODE>::stage;
                     tma_load_2d(stg, &tmK, &s.full_k[sk], kb * BK, tile * BM, pol_stream);
@@ -272,7 +231,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nkb; kb++, g++) {
                     const int sq = g % QST;
-                    KVQ_WAIT_COLD(&s.empty_a[sq], ((g / QST) & 1) ^ 1);  // released with the A stage
+                    mbar_wait_sleep(&s.empty_q[sq], ((g / QST) & 1) ^ 1);
                     mbar_arrive_tx(&s.full_q[sq], 2 * QTILE);
                     bulk_load(s.q[sq], p.qsplit + (size_t)kb * (2 * BN * BK), 2 * QTILE, &s.full_q[sq], pol_keep);
                 }
@@ -284,18 +243,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // DRAM read-modify-write) sit in code buffer grp & 1.  Store them with TMA; one block
             // later, when the bulk engine has read them out of smem, free the input stage for the
             // producer and (at group ends) the code buffer for the converters.
-            // (Measured alternative, scripts/probes/bw_mix2.cu: writing only the codes here and K_hat
-            // with a separate linear-grid dequantize reads the codes back for 10 B/elem in total; it
-            // loses to this 9 B/elem pass because the kernel then becomes issue-bound.)
             const uint64_t pol_out = (p.hints & 2) ? policy_evict_first() : policy_evict_normal();
             uint32_t g = 0, grp = 0;
             bool prev_group_end = false;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nkb; kb++, g++) {
                     const int sk = g % KST;
-                    KVQ_WAIT_COLD(&s.staged[sk], (g / KST) & 1);
+                    mbar_wait_sleep(&s.staged[sk], (g / KST) & 1);
                     tma_store_2d(&tmKh, s.buf + sk * Ring<MODE>::stage, kb * BK, tile * BM, pol_out);
-                    const bool group_end = (kb % CODE_KB) == CODE_KB - 1;
+                    const bool group_end = (kb % CODE_KB) == CODE_KB - 1 || kb == nkb - 1;
                     if (group_end)
                         tma_store_2d(&tmKq, s.buf + 128 * 1024 + (grp & 1) * KTILE, (kb / CODE_KB) * (BK * CODE_KB),
                                      tile * BM, pol_out);
@@ -310,97 +266,66 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
             bulk_wait<0>();  // all K_hat / code writes complete before the CTA retires
-        } else if (warp == 1) {
+        } else if (warp == 1 && lane == 0) {
             // ------------------------------------------------------------ MMA issuer
-            // The whole warp runs the loop (all loop state warp-uniform, so descriptors live in
-            // uniform registers) and one elected lane issues: per K-step j, E_hi x [Q_hi; Q_lo]
-            // (N = 128) and E_lo x Q_hi (N = 64) into the same accumulator columns [0, 64).
-            // Measured (scripts/probes/mma_probe3.cu): 384 cycles per K-block, the tensor-pipe
-            // bound, vs ~800 for 12 N = 64 MMAs issued by a single thread with 2-3 commits.
             uint32_t g = 0, gc = 0;
-#ifdef KVQ_TRACE
-            long long tw_acc = 0, tw_a = 0, tw_q = 0, t_iss = 0, t_all = clock64(), t0;
-#define TR_BEGIN t0 = clock64()
-#define TR_END(x) x += clock64() - t0
-#else
-#define TR_BEGIN
-#define TR_END(x)
-#endif
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nkb; kb++, g++) {
                     const int ab = gc & 1;
-                    const uint32_t d = tbase + ab * ACC_COLS;
+                    const uint32_t d = tbase + ab * BN;
                     const bool chunk_first = (kb % CHUNK_KB) == 0;
                     const bool chunk_last = (kb % CHUNK_KB) == CHUNK_KB - 1 || kb == nkb - 1;
                     if (chunk_first) {
-                        TR_BEGIN;
                         KVQ_WAIT_HOT(&s.empty_acc[ab], ((gc >> 1) & 1) ^ 1);
-                        TR_END(tw_acc);
+                        tc_fence_after();
                     }
-                    const int sa = g % AST;
-                    TR_BEGIN;
+                    const int sa = g % AST, sq = g % QST;
                     KVQ_WAIT_HOT(&s.full_a[sa], (g / AST) & 1);
-                    TR_END(tw_a);
-                    TR_BEGIN;
-                    KVQ_WAIT_HOT(&s.full_q[sa], (g / QST) & 1);
-                    TR_END(tw_q);
-                    TR_BEGIN;
+                    KVQ_WAIT_HOT(&s.full_q[sq], (g / QST) & 1);
                     tc_fence_after();
-                    if (elect_one()) {
-                        const uint32_t ahi = tbase + A_COL0 + sa * 64, alo = ahi + 32;
-                        const uint64_t b0 = smem_desc(smem_u32(s.q[sa]), 2048, 128);
+                    const uint32_t ahi = tbase + A_COL0 + sa * 64, alo = ahi + 32;
+                    const uint32_t qhi = smem_u32(s.q[sq]), qlo = qhi + QTILE;
 #pragma unroll
-                        for (int j = 0; j < ((p.hints & 4) ? 0 : BK / 8); j++) {  // hints bit 2: experiments only
-                            // K-step j covers k-groups 2j, 2j+1: +4096 B = +256 in descriptor units
-                            const uint64_t bj = b0 + (uint64_t)(256 * j);
-                            mma_tf32_ts(d, ahi + 8 * j, bj, IDESC2, (!chunk_first || j != 0) ? 1u : 0u);
-                            mma_tf32_ts(d, alo + 8 * j, bj, IDESC, 1);
-                        }
-                        mma_commit(&s.empty_a[sa]);  // frees the A stage and the Q stage
-                        if (chunk_last) mma_commit(&s.full_acc[ab]);
+                    for (int j = 0; j < BK / 8; j++) {
+                        // K-step j covers k-groups 2j, 2j+1 (LBO apart = 1024 B), 8-row groups 128 B apart
+                        const uint64_t bh = smem_desc(qhi + j * 2048, 1024, 128);
+                        const uint64_t bl = smem_desc(qlo + j * 2048, 1024, 128);
+                        mma_tf32_ts(d, ahi + 8 * j, bh, IDESC, (!chunk_first || j != 0) ? 1u : 0u);
+                        mma_tf32_ts(d, ahi + 8 * j, bl, IDESC, 1);
+                        mma_tf32_ts(d, alo + 8 * j, bh, IDESC, 1);
                     }
-                    __syncwarp();
-                    if (chunk_last) gc++;
-                    TR_END(t_iss);
+                    mma_commit(&s.empty_a[sa]);
+                    mma_commit(&s.empty_q[sq]);
+                    if (chunk_last) {
+                        mma_commit(&s.full_acc[ab]);
+                        gc++;
+                    }
                 }
             }
-#ifdef KVQ_TRACE
-            if (blockIdx.x == 0 && lane == 0)
-                printf("MMA issuer: total %lld  wait_acc %lld  wait_a %lld  wait_q %lld  issue %lld (cycles)\n",
-                       clock64() - t_all, tw_acc, tw_a, tw_q, t_iss);
-#endif
         }
     } else if (warp < EPI_W0) {
-        // ------------------------------------------------------------ converters (warps 4..EPI_W0-1)
-        // thread = (row r, part h): columns CPT*h .. CPT*h+CPT-1 of every 32-column K-block.
-        // 16 warps (4 per SM sub-partition) hide the per-element dependency chain (smem load ->
-        // quantize -> E -> split -> TMEM store) that 8 warps left exposed.
-        setmaxnreg_dec<REG_CONV>();
+        // ------------------------------------------------------------ converters (warps 4..11)
+        // thread = (row r, half h): columns 16h..16h+15 of every 32-column K-block
         const int quarter = warp & 3;
         const int h = (warp - CONV_W0) >> 2;
         const int r = quarter * 32 + lane;  // row of the tile == TMEM lane
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         double ss = 0.0;
         float mx = 0.0f;
-        uint32_t cgrp = 0;                 // code-group counter (same order as the store warp)
-        int sk = 0, sa = 0;                // K ring and A ring slots
-        uint32_t pk = 0, pa = 0;           // their phases
-        bool pending = false;              // TMEM stores of the previous K-block not yet handed to the MMA
-        int sa_prev = 0;
-        float blk = 0.0f;                  // sum e^2 over one code group (fp32), carried in fp64
+        uint32_t g = 0, cgrp = 0;  // K-block and code-group counters (same order as the store warp)
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            for (int kb = 0; kb < nkb; kb++) {
-                const bool group_end = (kb % CODE_KB) == CODE_KB - 1;
-                KVQ_WAIT_CONV(&s.full_k[sk], pk);
+            for (int kb = 0; kb < nkb; kb++, g++) {
+                const int sk = g % KST;
+                KVQ_WAIT_HOT(&s.full_k[sk], (g / KST) & 1);
                 const uint32_t kbase = smem_u32(s.buf + sk * Ring<MODE>::stage);
-                float e[CPT];
+                float e[16];
                 if (MODE != 2) {
                     const uint32_t hbase = kbase + KTILE;
 #pragma unroll
-                    for (int c = 0; c < CPT / 4; c++) {
-                        const float4 a = lds128(swz(kbase, r, (CPT / 4) * h + c));
+                    for (int c = 0; c < 4; c++) {
+                        const float4 a = lds128(swz(kbase, r, 4 * h + c));
                         float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
-                        if (has_khat) b = lds128(swz(hbase, r, (CPT / 4) * h + c));
+                        if (has_khat) b = lds128(swz(hbase, r, 4 * h + c));
                         e[4 * c + 0] = __fsub_rn(a.x, b.x);
                         e[4 * c + 1] = __fsub_rn(a.y, b.y);
                         e[4 * c + 2] = __fsub_rn(a.z, b.z);
@@ -408,48 +333,42 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                     mbar_arrive(&s.empty_k[sk]);
                 } else {
-                    // ---- a3 + a4 on the resident K row segment (Eq. 7, Eq. 8): the arithmetic and
-                    // exactness argument of quant_v4_kernel (device_common.cuh), with the clamp moved
-                    // off the fast path: every |fq| <= 127.25 rounds to |q| <= 127 on both sides, and
-                    // a larger quotient (or a near tie, or an exact-path column) sends the thread's
-                    // CPT elements through the IEEE-division path, which clamps.
-                    float x[CPT], v[CPT], xh[CPT];
+                    // ---- a3 + a4 on the resident K row segment (Eq. 7, Eq. 8); same arithmetic and
+                    // exactness argument as quant_v4_kernel (device_common.cuh)
+                    float x[16], v[16], xh[16];
 #pragma unroll
-                    for (int c = 0; c < CPT / 4; c++) {
-                        const float4 a = lds128(swz(kbase, r, (CPT / 4) * h + c));
+                    for (int c = 0; c < 4; c++) {
+                        const float4 a = lds128(swz(kbase, r, 4 * h + c));
                         x[4 * c + 0] = a.x;
                         x[4 * c + 1] = a.y;
                         x[4 * c + 2] = a.z;
                         x[4 * c + 3] = a.w;
                     }
-                    const uint32_t cqb = smem_u32(&s.cq[sk]) + CPT * h * 8;  // this part's CPT {s, y}
-                    float dmax = 0.0f, fmx = 0.0f;
+                    const uint32_t cqb = smem_u32(&s.cq[sk]) + 16 * h * 8;  // this half's 16 {s, y}
+                    float dmax = 0.0f;
 #pragma unroll
-                    for (int c2 = 0; c2 < CPT / 2; c2++) {
+                    for (int c2 = 0; c2 < 8; c2++) {
                         const float4 cq = lds128(cqb + 16 * c2);  // {s, y} of 2 columns (broadcast read)
 #pragma unroll
                         for (int u = 0; u < 2; u++) {
                             const int i = 2 * c2 + u;
                             const float sc = u ? cq.z : cq.x, y = u ? cq.w : cq.y;
-                            const float fq = __fmul_rn(x[i], y);
-                            const float vv = __fadd_rn(fq, kMagic);
+                            const float cl = fminf(fmaxf(__fmul_rn(x[i], y), -127.0f), 127.0f);
+                            const float vv = __fadd_rn(cl, kMagic);
                             const float rr = __fsub_rn(vv, kMagic);
-                            dmax = fmaxf(dmax, fabsf(__fsub_rn(fq, rr)));
-                            fmx = fmaxf(fmx, fabsf(fq));
+                            dmax = fmaxf(dmax, fabsf(__fsub_rn(cl, rr)));
                             v[i] = vv;
                             xh[i] = __fmul_rn(rr, sc);
                         }
                     }
-                    if (dmax > kDangerThr || fmx > 127.25f || s.cq[sk].any_exact) {
-                        // rare: a near-tie or out-of-range quotient, or an exact-path column
+                    if (dmax > kDangerThr || s.cq[sk].any_exact) {
+                        // rare: a near-tie quotient or an exact-path column -> IEEE division there
 #pragma unroll
-                        for (int i = 0; i < CPT; i++) {
-                            const float2 cy = s.cq[sk].c[CPT * h + i];
-                            const float fq = __fmul_rn(x[i], cy.y);
-                            const float cl = fminf(fmaxf(fq, -127.0f), 127.0f);
+                        for (int i = 0; i < 16; i++) {
+                            const float2 cy = s.cq[sk].c[16 * h + i];
+                            const float cl = fminf(fmaxf(__fmul_rn(x[i], cy.y), -127.0f), 127.0f);
                             const float rr = __fsub_rn(__fadd_rn(cl, kMagic), kMagic);
-                            if (fabsf(__fsub_rn(cl, rr)) > kDangerThr || fabsf(fq) > 127.25f ||
-                                (cy.y == 0.0f && cy.x != 0.0f)) {
+                            if (fabsf(__fsub_rn(cl, rr)) > kDangerThr || (cy.y == 0.0f && cy.x != 0.0f)) {
                                 const int cd = quant_exact(x[i], cy.x);
                                 v[i] = __fadd_rn((float)cd, kMagic);
                                 xh[i] = __fmul_rn((float)cd, cy.x);
@@ -459,70 +378,51 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     // K_hat overwrites x in the input stage (same swizzled positions, read by this
                     // thread only); the codes go to the group's code buffer.  The store warp writes
                     // both out with TMA and then frees the stage (and the code buffer).
-                    if ((kb % CODE_KB) == 0) KVQ_WAIT_CONV(&s.cstored[cgrp & 1], ((cgrp >> 1) & 1) ^ 1);
+                    if ((kb % CODE_KB) == 0) KVQ_WAIT_HOT(&s.cstored[cgrp & 1], ((cgrp >> 1) & 1) ^ 1);
                     const uint32_t cds = smem_u32(s.buf + 128 * 1024 + (cgrp & 1) * KTILE);
 #pragma unroll
-                    for (int c = 0; c < CPT / 4; c++)
-                        sts128(swz(kbase, r, (CPT / 4) * h + c),
+                    for (int c = 0; c < 4; c++)
+                        sts128(swz(kbase, r, 4 * h + c),
                                make_float4(xh[4 * c], xh[4 * c + 1], xh[4 * c + 2], xh[4 * c + 3]));
-                    // 8 codes = bytes 8h..8h+7 of the K-block's 32-byte segment of row r
-                    uint2 w;
+                    uint4 w;
                     w.x = pack4(v[0], v[1], v[2], v[3]);
                     w.y = pack4(v[4], v[5], v[6], v[7]);
-                    sts64u(swz(cds, r, (kb % CODE_KB) * 2 + (h >> 1)) + 8 * (h & 1), w);
+                    w.z = pack4(v[8], v[9], v[10], v[11]);
+                    w.w = pack4(v[12], v[13], v[14], v[15]);
+                    sts128u(swz(cds, r, (kb % CODE_KB) * 2 + h), w);
                     fence_proxy_async();  // generic smem writes -> visible to the TMA (async proxy)
                     mbar_arrive(&s.staged[sk]);
-                    if (group_end) cgrp++;
+                    if ((kb % CODE_KB) == CODE_KB - 1 || kb == nkb - 1) cgrp++;
 #pragma unroll
-                    for (int i = 0; i < CPT; i++) e[i] = __fsub_rn(x[i], xh[i]);  // exact (fact 4)
+                    for (int i = 0; i < 16; i++) e[i] = __fsub_rn(x[i], xh[i]);  // exact (fact 4)
                 }
                 if (MODE != 1) {
-                    // e^2 summed in fp32 over one code group (<= 4 * CPT terms), carried in fp64
+                    // e^2 summed over the 16 columns in fp32, blocks carried in fp64
+                    float blk = 0.0f;
 #pragma unroll
-                    for (int i = 0; i < CPT; i++) {
+                    for (int i = 0; i < 16; i++) {
                         blk = fmaf(e[i], e[i], blk);
                         mx = fmaxf(mx, fabsf(e[i]));
                     }
-                    if (group_end) {
-                        ss += (double)blk;
-                        blk = 0.0f;
-                    }
+                    ss += (double)blk;
                 }
                 // 3xTF32 split: hi = e with the 13 low mantissa bits cleared (a tf32 value),
                 // lo = e - hi exactly (the tensor core reads lo's top 11 bits: error <= 2^-21 |e|)
-                uint32_t hi[CPT], lo[CPT];
+                uint32_t hi[16], lo[16];
 #pragma unroll
-                for (int i = 0; i < CPT; i++) {
+                for (int i = 0; i < 16; i++) {
                     hi[i] = __float_as_uint(e[i]) & 0xFFFFE000u;
                     lo[i] = __float_as_uint(__fsub_rn(e[i], __uint_as_float(hi[i])));
                 }
-                // The previous block's TMEM stores have had a whole iteration to land: wait for them
-                // only now and hand that A stage to the MMA (keeps tcgen05.wait::st off the critical path).
-                if (pending) {
-                    tmem_wait_st();
-                    tc_fence_before();
-                    mbar_arrive(&s.full_a[sa_prev]);
-                }
-                KVQ_WAIT_CONV(&s.empty_a[sa], pa ^ 1);
+                const int sa = g % AST;
+                KVQ_WAIT_HOT(&s.empty_a[sa], ((g / AST) & 1) ^ 1);
                 tc_fence_after();
-                tmem_st8(tbase + lane_off + A_COL0 + sa * 64 + CPT * h, hi);
-                tmem_st8(tbase + lane_off + A_COL0 + sa * 64 + 32 + CPT * h, lo);
-                pending = true;
-                sa_prev = sa;
-                if (++sa == AST) {
-                    sa = 0;
-                    pa ^= 1;
-                }
-                if (++sk == KST) {
-                    sk = 0;
-                    pk ^= 1;
-                }
+                tmem_st16(tbase + lane_off + A_COL0 + sa * 64 + 16 * h, hi);
+                tmem_st16(tbase + lane_off + A_COL0 + sa * 64 + 32 + 16 * h, lo);
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(&s.full_a[sa]);
             }
-        }
-        if (pending) {
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&s.full_a[sa_prev]);
         }
         if (MODE != 1) {
             double mxd = (double)mx;
@@ -537,15 +437,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     } else {
         // ------------------------------------------------------------ epilogue (warps 12..15)
-        setmaxnreg_inc<REG_EPI>();
+        setmaxnreg_inc<200>();
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         double attn = 0.0;
         uint32_t gc = 0;
-#ifdef KVQ_TRACE
-        long long ew = 0, ed = 0, eall = clock64();
-#endif
         const int nchunks = (nkb + CHUNK_KB - 1) / CHUNK_KB;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             double acc[BN];
@@ -553,29 +450,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int j = 0; j < BN; j++) acc[j] = 0.0;
             for (int c = 0; c < nchunks; c++, gc++) {
                 const int ab = gc & 1;
-#ifdef KVQ_TRACE
-                const long long te0 = clock64();
-#endif
-                KVQ_WAIT_COLD(&s.full_acc[ab], (gc >> 1) & 1);
-#ifdef KVQ_TRACE
-                const long long te1 = clock64();
-                ew += te1 - te0;
-#endif
+                mbar_wait_sleep(&s.full_acc[ab], (gc >> 1) & 1);
                 tc_fence_after();
                 uint32_t v[32];
-                // columns [0, 64): E_hi.Q_hi + E_lo.Q_hi; [64, 128): E_hi.Q_lo -- both add into acc
 #pragma unroll
-                for (int hh = 0; hh < ACC_COLS / 32; hh++) {
-                    tmem_ld32(tbase + lane_off + ab * ACC_COLS + 32 * hh, v);
+                for (int hh = 0; hh < BN / 32; hh++) {
+                    tmem_ld32(tbase + lane_off + ab * BN + 32 * hh, v);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int j = 0; j < 32; j++) acc[(32 * hh) % BN + j] += (double)__uint_as_float(v[j]);
+                    for (int j = 0; j < 32; j++) acc[32 * hh + j] += (double)__uint_as_float(v[j]);
                 }
                 tc_fence_before();
                 mbar_arrive(&s.empty_acc[ab]);
-#ifdef KVQ_TRACE
-                ed += clock64() - te1;
-#endif
             }
             const int64_t row = (int64_t)tile * BM + r;
             if (row < T) {
@@ -590,10 +476,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
         }
-#ifdef KVQ_TRACE
-        if (blockIdx.x == 0 && lane == 0)
-            printf("epilogue warp %d: total %lld  wait_full_acc %lld  drain %lld\n", warp, clock64() - eall, ew, ed);
-#endif
         if (MODE != 1) {
             for (int o = 16; o > 0; o >>= 1) attn += __shfl_xor_sync(0xffffffffu, attn, o);
             if (lane == 0) s.red[1][quarter] = attn;
@@ -603,7 +485,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncthreads();
     if (MODE != 1 && threadIdx.x == 0) {
         Partial pt{0.0, 0.0, 0.0, 0.0};
-        for (int i = 0; i < NCONV_W; i++) {  // fixed order: deterministic
+        for (int i = 0; i < 8; i++) {  // fixed order: deterministic
             pt.sum_sq += s.red[0][i];
             pt.max_abs = fmax(pt.max_abs, s.red[2][i]);
         }
@@ -656,7 +538,7 @@ bool tc_eligible(const float *K, const float *K_hat, int64_t T, int64_t D, int64
            tc::encode_fn() != nullptr;
 }
 
-size_t tc_qsplit_bytes(int64_t D) { return (size_t)tc::nkb_of(D) * 2 * tc::QTILE; }
+size_t tc_qsplit_bytes(int64_t D) { return (size_t)((D + tc::BK - 1) / tc::BK) * 2 * tc::QTILE; }
 
 bool tc_roundtrip_eligible(const float *K, const int8_t *Kq, const float *K_hat, int64_t T, int64_t D, int64_t nq) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(K) | reinterpret_cast<uintptr_t>(Kq) |
@@ -664,7 +546,7 @@ bool tc_roundtrip_eligible(const float *K, const int8_t *Kq, const float *K_hat,
     return tc_eligible(K, K_hat, T, D, nq) && D % 16 == 0 && (a % 16) == 0;
 }
 
-size_t tc_colq_bytes(int64_t D) { return (size_t)tc::nkb_of(D) * sizeof(tc::ColRec); }
+size_t tc_colq_bytes(int64_t D) { return (size_t)((D + tc::BK - 1) / tc::BK) * sizeof(tc::ColRec); }
 
 template <int MODE>
 static void launch_mode(const CUtensorMap &mK, const CUtensorMap &mKh, const CUtensorMap &mKq, const tc::TcParams &p,
@@ -681,7 +563,7 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
                           int64_t nq, void *ws_q, void *partials, int *grid_out, float *S, cudaStream_t s,
                           const float *scales, void *ws_colq, int8_t *Kq_out, float *Kh_out) {
     using namespace tc;
-    const int64_t nkb = nkb_of(D);
+    const int64_t nkb = (D + BK - 1) / BK;
     const int ntiles = (int)((T + BM - 1) / BM);
     CUtensorMap mK, mKh, mKq;
     if (!make_map_f32(&mK, K, T, D)) return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(K) failed");

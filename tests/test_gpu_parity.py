@@ -75,7 +75,9 @@ def test_device_generator_matches_oracle(kvq, orc, dist):
 
 # ----------------------------------------------------------------------------- edge battery
 EDGE_SHAPES = [(1, 1), (1, 4), (1, 5), (2, 3), (3, 7), (7, 13), (64, 128), (1000, 13), (257, 127),
-               (129, 1024), (33, 4096), (5000, 8)]
+               (129, 1024), (33, 4096), (5000, 8),
+               # row-slab grid: column chunks of 256 float4 with a partial last chunk (D/4 = 257, 300)
+               (5, 1028), (33, 1200), (1, 1200)]
 
 
 @pytest.mark.parametrize("shape", EDGE_SHAPES)
@@ -388,7 +390,9 @@ def test_tc_and_simt_metrics_agree(kvq, orc, monkeypatch):
 
 # ----------------------------------------------------------------------------- single-pass roundtrip (a3+a4+a5+a6)
 RT_CASES = [(1, 16, 1), (128, 32, 64), (129, 48, 64), (1000, 1024, 64), (300, 128, 17), (257, 8192, 64),
-            (77, 13, 5), (100, 40, 70), (64, 64, 0)]
+            (77, 13, 5), (100, 40, 70), (64, 64, 0),
+            # K-blocks padded to a multiple of 4 (33 -> 36, 5 -> 8): zero-filled K boxes, clipped code stores
+            (130, 1040, 64), (131, 160, 9)]
 
 
 @pytest.mark.timeout(300)
