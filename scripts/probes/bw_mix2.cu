@@ -19,6 +19,7 @@
 using namespace kvq::tc;
 
 static const int64_t T = 131072, D = 8192, N = T * D;
+static int g_hints = getenv("HINTS") ? atoi(getenv("HINTS")) : 3;
 
 // ------------------------------------------------------------------ SIMT linear
 template <int UNR, int CS, int WC>
@@ -446,7 +447,7 @@ int main(int argc, char **argv) {
         const size_t smem = ST * BR * BC * 4 + 16384 + 1024;                                                     \
         cudaFuncSetAttribute(tile2d<ST, BC, WC, RW, BR, WD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         timeit(name, bpe, [&] {                                                                                  \
-            tile2d<ST, BC, WC, RW, BR, WD><<<sms, 64, smem>>>(mi, mo, mc, (int)(T / BR), (int)(D / BC), 3, 0);     \
+            tile2d<ST, BC, WC, RW, BR, WD><<<sms, 64, smem>>>(mi, mo, mc, (int)(T / BR), (int)(D / BC), g_hints, 0);     \
         });                                                                                                      \
     }
     const int ntl = (int)(T / 128), nkb = (int)(D / 32);
@@ -463,14 +464,61 @@ int main(int argc, char **argv) {
             tile_grp<8, G, IL><<<grid, 64, smem>>>(mi, mo, IL == 1 ? mc32 : mc128, ntl, nkb);                 \
         });                                                                                                    \
     }
+    if (getenv("DEPTH2")) {
+    TILE(2, 32, 128, 1, 3, "tile BR128 BC32 ST2   R4W5", 9);
+    TILE(3, 32, 128, 1, 3, "tile BR128 BC32 ST3   R4W5", 9);
+    TILE(4, 32, 128, 1, 3, "tile BR128 BC32 ST4   R4W5", 9);
+    TILE(5, 32, 128, 1, 3, "tile BR128 BC32 ST5   R4W5", 9);
+    TILE(6, 32, 128, 1, 3, "tile BR128 BC32 ST6   R4W5", 9);
+    TILE(8, 32, 128, 1, 3, "tile BR128 BC32 ST8   R4W5", 9);
+    TILE(3, 32, 128, 0, 2, "tile BR128 BC32 ST3   W4 only", 4);
+    TILE(4, 32, 128, 0, 2, "tile BR128 BC32 ST4   W4 only", 4);
+    TILE(8, 32, 128, 0, 2, "tile BR128 BC32 ST8   W4 only", 4);
+    printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+    return 0;
+    }
+    if (getenv("DEPTH")) {
+    TILE(4, 32, 128, 1, 3, "tile BR128 BC32 ST4   R4W5", 9);
+    TILE(6, 32, 128, 1, 3, "tile BR128 BC32 ST6   R4W5", 9);
+    TILE(8, 32, 128, 1, 3, "tile BR128 BC32 ST8   R4W5", 9);
+    TILE(10, 32, 128, 1, 3, "tile BR128 BC32 ST10  R4W5", 9);
+    TILE(12, 32, 128, 1, 3, "tile BR128 BC32 ST12  R4W5", 9);
+    TILEW(8, 32, 128, 1, 3, 2, "tile BR128 BC32 ST8 WD2  R4W5", 9);
+    TILEW(10, 32, 128, 1, 3, 2, "tile BR128 BC32 ST10 WD2 R4W5", 9);
+    TILEW(12, 32, 128, 1, 3, 3, "tile BR128 BC32 ST12 WD3 R4W5", 9);
+    printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+    return 0;
+    }
+    if (getenv("GRP")) {
     GRP(1, 4, "tile grp G1 IL4 (current)  R4W5");
     GRP(2, 4, "tile grp G2 IL4            R4W5");
     GRP(4, 4, "tile grp G4 IL4            R4W5");
     GRP(8, 4, "tile grp G8 IL4            R4W5");
+    GRP(2, 1, "tile grp G2 IL1            R4W5");
     GRP(4, 1, "tile grp G4 IL1            R4W5");
     GRP(8, 1, "tile grp G8 IL1            R4W5");
     GRP(16, 1, "tile grp G16 IL1           R4W5");
     GRP(37, 1, "tile grp G37 IL1           R4W5");
+    GRP(74, 1, "tile grp G74 IL1           R4W5");
+    printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+    return 0;
+    }
+    // round-1 session 3: tile height (rows written concurrently per CTA) and store L2 policy
+    TILE(8, 32, 128, 1, 3, "tile BR128 BC32 (current)   R4W5", 9);
+    TILE(16, 32, 64, 1, 3, "tile BR64  BC32             R4W5", 9);
+    TILE(32, 32, 32, 1, 3, "tile BR32  BC32             R4W5", 9);
+    TILE(64, 32, 16, 1, 3, "tile BR16  BC32             R4W5", 9);
+    TILE(8, 32, 128, 0, 3, "tile BR128 BC32 no codes    R4W4", 8);
+    TILE(16, 32, 64, 0, 3, "tile BR64  BC32 no codes    R4W4", 8);
+    TILE(32, 32, 32, 0, 3, "tile BR32  BC32 no codes    R4W4", 8);
+    TILE(8, 32, 128, 0, 2, "tile BR128 BC32 write only  W4", 4);
+    TILE(16, 32, 64, 0, 2, "tile BR64  BC32 write only  W4", 4);
+    TILE(32, 32, 32, 0, 2, "tile BR32  BC32 write only  W4", 4);
+    TILE(64, 32, 16, 0, 2, "tile BR16  BC32 write only  W4", 4);
+    {
+        const int64_t nb = N / (256 * 2 * 4);
+        timeit("linear grid R4W5 (reference)", 9, [&] { lin_grid<2, 1, 1><<<nb, 256>>>(in4, ok4, oc4, n4); });
+    }
     printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
     return 0;
 }
