@@ -419,6 +419,7 @@ static void timeit(const char *name, double bpe, F launch) {
 }
 
 int main(int argc, char **argv) {
+    setvbuf(stdout, nullptr, _IONBF, 0);
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     float *in, *ok;
@@ -463,6 +464,23 @@ int main(int argc, char **argv) {
         timeit(name, 9, [&] {                                                                                  \
             tile_grp<8, G, IL><<<grid, 64, smem>>>(mi, mo, IL == 1 ? mc32 : mc128, ntl, nkb);                 \
         });                                                                                                    \
+    }
+    if (getenv("WIDE")) {
+    TILE(8, 32, 128, 1, 3, "tile BR128 BC32  ST8  R4W5", 9);
+    TILE(4, 32, 128, 1, 3, "tile BR128 BC32  ST4  R4W5", 9);
+    TILE(2, 64, 128, 1, 3, "tile BR128 BC64  ST2  R4W5", 9);
+    TILE(3, 64, 128, 1, 3, "tile BR128 BC64  ST3  R4W5", 9);
+    TILE(4, 64, 128, 1, 3, "tile BR128 BC64  ST4  R4W5", 9);
+    TILE(6, 64, 128, 1, 3, "tile BR128 BC64  ST6  R4W5", 9);
+    TILE(2, 128, 128, 1, 3, "tile BR128 BC128 ST2  R4W5", 9);
+    TILE(3, 128, 128, 1, 3, "tile BR128 BC128 ST3  R4W5", 9);
+    TILE(1, 256, 128, 1, 3, "tile BR128 BC256 ST1  R4W5", 9);
+    TILE(4, 128, 64, 1, 3, "tile BR64  BC128 ST4  R4W5", 9);
+    TILE(2, 256, 64, 1, 3, "tile BR64  BC256 ST2  R4W5", 9);
+    TILE(4, 256, 32, 1, 3, "tile BR32  BC256 ST4  R4W5", 9);
+    TILE(8, 256, 16, 1, 3, "tile BR16  BC256 ST8  R4W5", 9);
+    printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+    return 0;
     }
     if (getenv("DEPTH2")) {
     TILE(2, 32, 128, 1, 3, "tile BR128 BC32 ST2   R4W5", 9);

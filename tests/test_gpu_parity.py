@@ -388,6 +388,50 @@ def test_tc_and_simt_metrics_agree(kvq, orc, monkeypatch):
     assert kvq.kvq_error_metrics(Kd, kh, Qd, s) == kvq.kvq_error_metrics(Kd, kh, Qd, s)
 
 
+# ----------------------------------------------------------------------------- the headline step at C3 / C4
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_roundtrip_config_large_parity(kvq, orc, cfg):
+    """bench.py's step in its own launch configuration (kvq_compute_scales, then
+    kvq_roundtrip with caller workspace and device metrics, nq = 64 over all T
+    rows) at full size: codes / K_hat hash-equal the SURVEY goldens (independent
+    numpy), sampled rows equal the oracle bit for bit, L2 / max-abs match the
+    goldens and the attention error matches the oracle's all-rows value
+    (tests/golden/oracle_attn.json, written by scripts/oracle_goldens.py from
+    oracle/ only) within 1e-5."""
+    g = gold(cfg)
+    with open(os.path.join(GOLD, "oracle_attn.json")) as f:
+        ga = json.load(f)[cfg]
+    T, D, nq = g["T"], g["D"], 64
+    Kd = kvq.kvq_synth_fill(T, D, seed=42)
+    Qd = kvq.kvq_synth_fill(nq, D, seed=43)
+    s = torch.empty(D, dtype=torch.float32, device="cuda")
+    Kq = torch.empty(T, D, dtype=torch.int8, device="cuda")
+    Kh = torch.empty(T, D, dtype=torch.float32, device="cuda")
+    ws = torch.empty(kvq.kvq_roundtrip_workspace_size(T, D, nq), dtype=torch.uint8, device="cuda")
+    mout = torch.empty(kvq.METRICS_BYTES, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+    kvq.kvq_compute_scales(Kd, s, stream=st)
+    kvq.kvq_roundtrip(Kd, s, Qd, Kq, Kh, out_dev=mout, workspace=ws, stream=st)
+    m = kvq.metrics_from_device(mout)
+    sh = host(s)
+    assert hashlib.sha256(sh.tobytes()).hexdigest()[:16] == g["scales_sha16"]
+    assert hashlib.sha256(host(Kq).tobytes()).hexdigest()[:16] == g["q_sha16"]
+    hk = hashlib.sha256()
+    for r0 in range(0, T, 8192):
+        hk.update(host(Kh[r0:r0 + 8192]).tobytes())
+    assert hk.hexdigest()[:16] == g["khat_sha16"]
+    assert _rel(m["l2"], g["l2"]) <= REL and m["max_abs"] == g["max_abs"]
+    assert m["theoretical_max"] == orc.theoretical_max(sh)
+    assert _rel(m["attn_mean_abs"], ga["attn_mean_abs"]) <= REL
+    rng = np.random.default_rng(1)
+    for r in np.sort(rng.choice(T, 32, replace=False)):
+        Kr = orc.fill(1, D, 42, 0, int(r))
+        qo = orc.quantize(Kr, sh)  # sh == the oracle's scales: its hash equals the golden above
+        same_bits(host(Kq[r:r + 1]), qo)
+        same_bits(host(Kh[r:r + 1]), orc.dequantize(qo, sh))
+
+
 # ----------------------------------------------------------------------------- single-pass roundtrip (a3+a4+a5+a6)
 RT_CASES = [(1, 16, 1), (128, 32, 64), (129, 48, 64), (1000, 1024, 64), (300, 128, 17), (257, 8192, 64),
             (77, 13, 5), (100, 40, 70), (64, 64, 0),

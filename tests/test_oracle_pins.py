@@ -367,3 +367,19 @@ def test_survey_golden_hashes_and_metrics(orc, cfg):
         K = orc.fill(T, D)
         s, q, Kh = orc.roundtrip(K)
         assert hashlib.sha256(q.tobytes()).hexdigest() == r["q_sha"]
+
+
+def test_oracle_attn_goldens_file():
+    """tests/golden/oracle_attn.json (scripts/oracle_goldens.py, oracle/ only) agrees with the
+    independent numpy values of the SURVEY appendix where those exist (C1, C2), and its C3/C4
+    values with the closed form sqrt(2/pi) * mean(s) * sqrt(D/36) and the paper's 0.095."""
+    ga = gold("oracle_attn.json")
+    sv = gold("survey_appendix.json")
+    for cfg in ("C1", "C2"):
+        assert ga[cfg]["attn_mean_abs"] == pytest.approx(sv[cfg]["attn_mean_abs"], rel=1e-12)
+    for cfg in ("C3", "C4"):
+        g = ga[cfg]
+        assert g["attn_mean_abs"] == pytest.approx(g["attn_abs_sum"] / (g["nq"] * g["T"]), rel=1e-15)
+        closed = math.sqrt(2 / math.pi) * (1 / 127) * math.sqrt(g["D"] / 36)
+        assert g["attn_mean_abs"] == pytest.approx(closed, rel=0.01)
+        assert abs(g["attn_mean_abs"] - 0.095) < 0.002
