@@ -173,9 +173,11 @@ kvq_status kvq_quantize_dequantize(const float *K, const float *scales, int64_t 
 /* a1+a2+a3+a4 in ONE cooperative launch (single GPU, D % 4 == 0, aligned): the
  * column max pass pulls K into the 126 MB L2, a grid-wide barrier, then each
  * thread forms its own columns' scales and quantizes + dequantizes the same
- * elements (from L2 when K fits).  Results are bit-identical to
+ * elements from L2.  Results are bit-identical to
  * kvq_compute_scales + kvq_quantize_dequantize, which is what runs otherwise
- * (comm != NULL, unaligned, or no co-resident grid).  workspace: device scratch
+ * (K larger than 3/4 of the L2 or D < 256 -- where the two streaming passes are
+ * faster, measured crossover in profiles/r01/sweep_c5.md --, comm != NULL,
+ * unaligned, or no co-resident grid).  workspace: device scratch
  * of kvq_quantize_fused_workspace_size(T, D) bytes.  *single_pass_out [host,
  * nullable] reports which path ran. */
 size_t kvq_quantize_fused_workspace_size(int64_t T, int64_t D);

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -57,7 +58,7 @@ kvq_status device_ok() {
             cudaGetLastError();
             return fail(KVQ_ERR_CUDA, "cudaGetDeviceProperties failed");
         }
-        g_info[dev] = DeviceInfo{dev, p.multiProcessorCount, p.major, p.minor};
+        g_info[dev] = DeviceInfo{dev, p.multiProcessorCount, p.major, p.minor, (int64_t)p.l2CacheSize};
         cudaFuncAttributes fa;
         bool image = cudaFuncGetAttributes(&fa, probe_kernel) == cudaSuccess;
         cudaGetLastError();
@@ -294,7 +295,14 @@ extern "C" kvq_status kvq_quantize_fused(const float *K, int64_t T, int64_t D, f
     KVQ_TRY(device_ok());
     cudaStream_t s = (cudaStream_t)stream;
     if (single_pass_out) *single_pass_out = 0;
-    if (!comm) {
+    // The single pass pays off only while its second phase re-reads K from L2: measured crossover
+    // (C5 sweep, profiles/r01/sweep_c5.md) between 0.5 and 1 L2 of K for D >= 1024, never for D = 128.  Beyond
+    // that the two streaming passes (row-slab quantize+dequantize) are faster.  KVQ_FUSED_FORCE_SINGLE=1
+    // (tests only) keeps the single pass for every shape it supports.
+    const char *force_env = std::getenv("KVQ_FUSED_FORCE_SINGLE");
+    const bool force_single = force_env && std::atoi(force_env) == 1;
+    const bool l2_resident = D >= 256 && (int64_t)n * 4 <= device_info().l2_bytes / 4 * 3;
+    if (!comm && (l2_resident || force_single)) {
         kvq_status st = launch_single_pass(K, T, D, scales, Kq, K_hat, workspace, s);
         if (st == KVQ_OK) {
             if (single_pass_out) *single_pass_out = 1;
@@ -302,7 +310,7 @@ extern "C" kvq_status kvq_quantize_fused(const float *K, int64_t T, int64_t D, f
         }
         if (st != KVQ_ERR_UNSUPPORTED) return st;
     }
-    // two passes (sharded input, too large for one co-resident grid, or unaligned)
+    // two passes (sharded input, K not L2-resident, D < 256, too large for one co-resident grid, or unaligned)
     KVQ_TRY(kvq_compute_scales(K, T, D, scales, comm, stream));
     return launch_quantize(K, scales, T, D, Kq, K_hat, s);
 }

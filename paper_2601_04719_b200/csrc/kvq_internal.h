@@ -21,6 +21,7 @@ struct DeviceInfo {
     int device;
     int num_sms;
     int cc_major, cc_minor;
+    int64_t l2_bytes;
 };
 const DeviceInfo &device_info();
 

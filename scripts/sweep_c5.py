@@ -53,10 +53,15 @@ def main():
 
             single_flag = {}
 
-            def single_pass():
+            def single_pass():  # the cooperative kernel on every shape it supports
+                os.environ["KVQ_FUSED_FORCE_SINGLE"] = "1"
                 single_flag["v"] = kvq.kvq_quantize_fused(K, s, q, kh, workspace=ws, stream=stream)[3]
+                del os.environ["KVQ_FUSED_FORCE_SINGLE"]
 
-            for name, fn in (("two_pass", two_pass), ("single_pass", single_pass)):
+            def fused_auto():  # kvq_quantize_fused's own choice (single pass only while K is L2-resident)
+                single_flag["auto"] = kvq.kvq_quantize_fused(K, s, q, kh, workspace=ws, stream=stream)[3]
+
+            for name, fn in (("two_pass", two_pass), ("single_pass", single_pass), ("fused_auto", fused_auto)):
                 for cold in (True, False):
                     for _ in range(3):
                         fn()
@@ -75,7 +80,8 @@ def main():
                     r = {"D": D, "T": T, "N": N, "pipeline": name, "l2": "cold" if cold else "warm",
                          "ms": ms, "elements_per_s": N / (ms * 1e-3), "algo_GBps_13B": algo / (ms * 1e-3) / 1e9,
                          "frac_of_measured_hbm": algo / (ms * 1e-3) / 1e9 / peak,
-                         "single_pass_ran": single_flag.get("v") if name == "single_pass" else None,
+                         "single_pass_ran": (single_flag.get("v") if name == "single_pass" else
+                                             single_flag.get("auto") if name == "fused_auto" else None),
                          "K_MB": 4 * N / 1e6}
                     rows.append(r)
                     print(json.dumps(r), flush=True)
@@ -88,17 +94,22 @@ def main():
         f.write("# C5 sweep: single-pass fused vs two-pass (a1..a4), B200, median of %d\n\n" % a.iters)
         f.write("GB/s use the method's 13 algorithmic bytes/element (4 for a1 + 9 for a3+a4) for both "
                 "pipelines; above the HBM peak means L2 reuse.\n\n")
-        f.write("| D | N | K MB | L2 | two-pass ms | single-pass ms | two-pass GB/s | single-pass GB/s | speed-up |\n")
-        f.write("|---|---|---|---|---|---|---|---|---|\n")
+        f.write("`kvq_quantize_fused` (auto) runs the single pass only where K is L2-resident (D >= 256 and K <= 3/4 of "
+                "the L2), else the two passes.\n\n")
+        f.write("| D | N | K MB | L2 | two-pass ms | single-pass ms | two-pass GB/s | single-pass GB/s | speed-up | "
+                "fused auto ms (path) |\n")
+        f.write("|---|---|---|---|---|---|---|---|---|---|\n")
         for D in (128, 1024, 8192):
             for k in range(a.kmin, a.kmax + 1):
                 for l2 in ("cold", "warm"):
                     sel = {r["pipeline"]: r for r in rows if r["D"] == D and r["N"] == 1 << k and r["l2"] == l2}
-                    if len(sel) < 2:
+                    if len(sel) < 3:
                         continue
-                    t2, t1 = sel["two_pass"], sel["single_pass"]
+                    t2, t1, ta = sel["two_pass"], sel["single_pass"], sel["fused_auto"]
+                    path = "single" if ta["single_pass_ran"] else "two-pass"
                     f.write(f"| {D} | 2^{k} | {t2['K_MB']:.0f} | {l2} | {t2['ms']:.4f} | {t1['ms']:.4f} | "
-                            f"{t2['algo_GBps_13B']:.0f} | {t1['algo_GBps_13B']:.0f} | {t2['ms'] / t1['ms']:.2f} |\n")
+                            f"{t2['algo_GBps_13B']:.0f} | {t1['algo_GBps_13B']:.0f} | {t2['ms'] / t1['ms']:.2f} | "
+                            f"{ta['ms']:.4f} ({path}) |\n")
 
 
 if __name__ == "__main__":

@@ -511,10 +511,19 @@ def test_roundtrip_matches_separate_calls_C2(kvq, orc):
 @pytest.mark.parametrize("T,D,expect_single", [(1, 4, True), (1000, 128, True), (8192, 1024, True),
                                                (333, 8192, True), (77, 13, False), (4096, 4, True),
                                                (1 << 20, 128, True)])
-def test_quantize_fused_single_pass(kvq, orc, T, D, expect_single):
+@pytest.mark.parametrize("force", [True, False])
+def test_quantize_fused_single_pass(kvq, orc, monkeypatch, T, D, expect_single, force):
+    """expect_single: the cooperative single pass supports the shape.  By default it only runs where
+    K stays L2-resident (D >= 256 and K <= 3/4 of the L2, the measured crossover); the test-only
+    KVQ_FUSED_FORCE_SINGLE=1 runs it on every supported shape.  Bit-exact either way."""
+    if force:
+        monkeypatch.setenv("KVQ_FUSED_FORCE_SINGLE", "1")
+    else:
+        monkeypatch.delenv("KVQ_FUSED_FORCE_SINGLE", raising=False)
     K = orc.fill(T, D, 12, 1)
     s, q, kh, single = kvq.kvq_quantize_fused(dev(K))
-    assert single == expect_single
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    assert single == (expect_single and (force or (D >= 256 and T * D * 4 <= l2 // 4 * 3)))
     so, qo, kho = orc.roundtrip(K)
     same_bits(host(s), so)
     same_bits(host(q), qo)
@@ -522,8 +531,9 @@ def test_quantize_fused_single_pass(kvq, orc, T, D, expect_single):
 
 
 @pytest.mark.timeout(300)
-def test_quantize_fused_repeat_and_special_columns(kvq, orc):
+def test_quantize_fused_repeat_and_special_columns(kvq, orc, monkeypatch):
     """Workspace reuse across calls (counter/bits re-zeroed), zero and subnormal columns."""
+    monkeypatch.setenv("KVQ_FUSED_FORCE_SINGLE", "1")
     rng = np.random.default_rng(4)
     K = rng.uniform(-1, 1, (2048, 64)).astype(np.float32)
     K[:, 3] = 0.0
