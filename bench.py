@@ -180,7 +180,7 @@ def run_kvq(args, cfg, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2601_04719_b200 import kvq
-    from paper_2601_04719_b200.dist import make_comm, max_over_ranks, shard_rows
+    from paper_2601_04719_b200.dist import make_comm, make_peer, max_over_ranks, shard_rows
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -190,6 +190,24 @@ def run_kvq(args, cfg, rank, world, local_rank):
     # Under torchrun (even with one process) the NCCL exchange path is exercised:
     # kvq_compute_scales all-reduces the column maxima, the metrics their partials.
     comm = make_comm(rank, world) if dist.is_available() and dist.is_initialized() else None
+    # a7 (the scale all-reduce MAX): "peer" = kvq_compute_scales_peer, column max + exchange over
+    # CUDA-IPC peer memory + finalize in ONE kernel; "nccl" = column-max kernel, ncclAllReduce(MAX),
+    # finalize kernel.  (Without torchrun there is nothing to exchange: kvq_compute_scales.)
+    peer = None
+    a7 = "none" if comm is None else args.a7
+    if a7 == "peer" and args.format == "int8":
+        try:
+            peer = make_peer(rank, world, cfg["D"])
+        except Exception as e:  # e.g. no peer access between the GPUs: keep the NCCL exchange
+            a7 = f"nccl (peer setup failed: {str(e)[:80]})"
+    elif a7 == "peer":
+        a7 = "nccl (peer path is int8 only)"
+
+    def compute_scales():
+        if peer is not None:
+            kvq.kvq_compute_scales_peer(K, peer, scales, stream=stream)
+        else:
+            kvq.kvq_compute_scales(K, scales, comm=comm, stream=stream)
     stream = torch.cuda.current_stream()
 
     # device-resident inputs (generated on the GPU by the seeded counter RNG; rank r makes its rows)
@@ -205,7 +223,7 @@ def run_kvq(args, cfg, rank, world, local_rank):
         """The four separate ABI calls (a1+a2+a7, a3, a4, a5+a6): 22 B/elem."""
         if ev is not None:
             ev[0].record(stream)
-        kvq.kvq_compute_scales(K, scales, comm=comm, stream=stream)
+        compute_scales()
         if ev is not None:
             ev[1].record(stream)
         kvq.kvq_quantize(K, scales, Kq, stream=stream)
@@ -222,7 +240,7 @@ def run_kvq(args, cfg, rank, world, local_rank):
         """kvq_compute_scales (a1+a2+a7) then kvq_roundtrip (a3+a4+a5+a6 in one pass): 13 B/elem."""
         if ev is not None:
             ev[0].record(stream)
-        kvq.kvq_compute_scales(K, scales, comm=comm, stream=stream)
+        compute_scales()
         if ev is not None:
             ev[1].record(stream)
         kvq.kvq_roundtrip(K, scales, Q, Kq, Kh, out_dev=mout, workspace=ws, comm=comm, stream=stream)
@@ -354,6 +372,10 @@ def run_kvq(args, cfg, rank, world, local_rank):
                "api": "kvq_roundtrip_host_async x2 streams (pinned host K/Q -> scales, codes, metrics)",
                "attn_mean_abs": m_last["attn_mean_abs"]}
 
+    if peer is not None:
+        torch.cuda.synchronize()
+        dist.barrier()
+        peer.destroy()
     if comm is not None:
         comm.destroy()
     if rank != 0:
@@ -394,11 +416,12 @@ def run_kvq(args, cfg, rank, world, local_rank):
                    "pipeline": args.pipeline, "format": args.format,
                    "l2_flush": "none needed: inputs larger than L2 (K alone is %.2f GB > 126 MB)" % (4 * T * D / 1e9)
                    if 4 * T * D > 2 * 126e6 else "inputs L2-resident (warm)",
-                   "parallelism": f"token-shard x{world}", "comm": "nccl (libkvq kvq_comm_t)" if comm else None},
+                   "parallelism": f"token-shard x{world}", "comm": "nccl (libkvq kvq_comm_t)" if comm else None, "a7": a7},
         "hbm": {"GBps": algo_bytes / (ms * 1e-3) / 1e9 / world, "algo_bytes_per_elem": algo_per_elem,
                 "frac_of_peak_per_gpu": algo_bytes / (ms * 1e-3) / 1e9 / world / pk["hbm_gbs"]},
         "passes": pass_report, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": (7 if args.format != "int8" else 7 if args.pipeline == "fused" else 8) * args.steps, "clocks": clk.summary(wall0, wall1),
+        "gpu_launches": ((7 if args.format != "int8" else 7 if args.pipeline == "fused" else 8)
+                         - (1 if peer is not None else 0)) * args.steps, "clocks": clk.summary(wall0, wall1),
         "fidelity": {k: metrics[k] for k in ("l2", "max_abs", "attn_mean_abs", "theoretical_max")},
     }
     print(json.dumps(line), flush=True)
@@ -415,6 +438,9 @@ def main():
     ap.add_argument("--format", default="int8", choices=["int8", "e4m3", "int4", "int2"],
                     help="int8 = the paper's method (headline); e4m3 = the FP8 variant (NEXT-1); "
                          "int4 / int2 = the packed low-bit variants (NEXT-3)")
+    ap.add_argument("--a7", default="peer", choices=["peer", "nccl"],
+                    help="scale all-reduce under torchrun: peer = one fused kernel over CUDA-IPC peer memory "
+                         "(kvq_compute_scales_peer), nccl = ncclAllReduce between the column-max and finalize kernels")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=6)

@@ -56,6 +56,9 @@ typedef enum { KVQ_FMT_INT8 = 0, KVQ_FMT_E4M3 = 1, KVQ_FMT_INT4 = 2, KVQ_FMT_INT
 /* Opaque multi-GPU communicator (wraps an ncclComm_t; NULL = single GPU). */
 typedef struct kvq_comm_s *kvq_comm_t;
 
+/* Opaque peer-memory exchange (library-owned device buffer shared over CUDA IPC). */
+typedef struct kvq_peer_s *kvq_peer_t;
+
 /* Result of the paper's fidelity checks. */
 typedef struct {
     double l2;              /* sqrt(sum (K - K_hat)^2), unnormalised Frobenius norm (reading Q9) */
@@ -184,6 +187,28 @@ size_t kvq_quantize_fused_workspace_size(int64_t T, int64_t D);
 kvq_status kvq_quantize_fused(const float *K, int64_t T, int64_t D, float *scales, int8_t *Kq,
                               float *K_hat, void *workspace, size_t workspace_bytes, kvq_comm_t comm,
                               int *single_pass_out, void *stream);
+
+/* a1 + a7 + a2 in ONE kernel over peer memory, without NCCL (
+ * the all-reduce MAX of the column maxima).  Setup, once per rank:
+ *   kvq_peer_init(&p, nranks, rank, D, handle)  allocates this rank's exchange buffer
+ *     (library-owned, 2 x nranks x D u32 + flags) and writes its CUDA IPC handle
+ *     (kvq_peer_handle_bytes() bytes, [host]) for the caller to all-gather;
+ *   kvq_peer_open(p, handles)  maps every other rank's buffer ([host] nranks handles
+ *     in rank order; needs peer access between the GPUs, or one GPU).
+ * kvq_compute_scales_peer: K is this rank's token shard [T][D] (T may be 0), D % 4 == 0,
+ * K and scales 16-byte aligned.  Each CTA reduces its share into `scales` (abs bits);
+ * the last CTA pushes the local D-vector into every rank's buffer (P2P stores), raises
+ * an epoch flag in each (system-scope release), waits for all ranks' flags, takes the
+ * max over ranks and writes scales[d] = fl32(m_d / 127) (Eq. 5/6).  Scales are
+ * global and bit-identical to kvq_compute_scales over the whole matrix.  Every rank
+ * must make the same sequence of calls, and the ranks' kernels must be able to run
+ * concurrently (the last CTA waits for its peers).  kvq_peer_destroy: after all ranks'
+ * last call has completed (collective, like ncclCommDestroy). */
+size_t kvq_peer_handle_bytes(void);
+kvq_status kvq_peer_init(kvq_peer_t *out, int nranks, int rank, int64_t D, void *handle_out);
+kvq_status kvq_peer_open(kvq_peer_t p, const void *handles);
+kvq_status kvq_peer_destroy(kvq_peer_t p);
+kvq_status kvq_compute_scales_peer(const float *K, int64_t T, int64_t D, float *scales, kvq_peer_t p, void *stream);
 
 /* a5+a6: the paper's fidelity checks.
  * K, K_hat: [T][D] float32 in.  Q: [nq][D] float32 queries or NULL (nq == 0).

@@ -1,0 +1,285 @@
+// peer.cu — a1 + a7 + a2 in ONE kernel over peer memory (the
+// scale all-reduce without NCCL).
+//
+// Token-sharded ranks (one GPU each) need the global column max m_d = MAX_r m_d^(r)
+// (Eq. 6 over the whole matrix; the max is order-free) before
+// any rank can form s_d = m_d / 127 (Eq. 5/6).  Instead of column-max kernel
+// -> ncclAllReduce(MAX) -> finalize kernel, each rank runs one kernel:
+//   1. every CTA reduces its share of the local shard into `bits` (the same
+//      column-owning 128-bit streaming loop as colmax_v4_kernel, atomicMax of the
+//      abs bits);
+//   2. the LAST CTA to finish (grid-wide ticket) pushes the local D-vector straight
+//      into slot `rank` of every rank's exchange buffer (P2P stores over NVLink into
+//      buffers mapped with CUDA IPC), publishes an epoch flag in every rank's buffer
+//      (system-scope release), waits for the flags of all ranks (system-scope
+//      acquire), then takes the max over the R slots of its own buffer and writes
+//      s_d = fl32(m_d / divisor) for all d.
+// No host round trip and no collective library call: the exchange (R x D x 4 bytes
+// per rank, 32 KB per peer at D = 8192) overlaps the tail of the column-max pass of
+// the slower ranks.  Slots are double-buffered by epoch parity: a fast rank can be
+// at most one epoch ahead (it needs every rank's flag of epoch e to finish e), so
+// epoch e+1 never overwrites the slots a slow rank is still reading for epoch e.
+//
+// Bit-exact with kvq_compute_scales (+NCCL) and the oracle: max is exact in any
+// order.  Every rank must call kvq_compute_scales_peer the same number of times in
+// the same order (like NCCL), and the ranks' kernels must be able to run
+// concurrently (one GPU per rank, or time-sliced processes on one GPU in tests).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "device_common.cuh"
+#include "kvq_internal.h"
+
+constexpr int kPeerMax = 16;
+
+struct PeerArgs {
+    uint32_t *bufs[kPeerMax];  // every rank's exchange buffer (bufs[rank] = this rank's own)
+    unsigned *ticket;          // grid-wide ticket (this rank's buffer)
+    int nranks, rank;
+    int64_t D, slot_stride;    // u32 per slot (D rounded up to 64)
+    uint64_t epoch;
+    float divisor;
+};
+
+// exchange buffer layout (u32 units): [flags: kPeerMax x u64 = 32 u32][ticket: 1 u32, pad to 64][slots: 2 x R x S]
+constexpr int64_t kFlagsU32 = 2 * kPeerMax, kHdrU32 = 64;
+
+struct kvq_peer_s {
+    int nranks, rank, device;
+    int64_t D;
+    uint32_t *local;                 // library-owned (cudaMalloc), shared with the peers over CUDA IPC
+    uint32_t *mapped[kPeerMax];      // peer buffers opened with cudaIpcOpenMemHandle (own slot: nullptr)
+    uint32_t *bufs[kPeerMax];
+    uint64_t epoch;
+    bool open;
+};
+
+namespace kvq {
+
+__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int U>
+__global__ void __launch_bounds__(kThreads, 6) colmax_peer_kernel(const float4 *__restrict__ K, int64_t n4,
+                                                               int64_t cols4, int64_t G, uint32_t *bits,
+                                                               const __grid_constant__ PeerArgs pa) {
+    // ---- 1. local column max of this rank's shard (as colmax_v4_kernel, without the smem stage)
+    const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (g < G) {
+        uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+        int64_t i = g;
+        for (; i + (U - 1) * G < n4; i += U * G) {
+            float4 v[U];
+#pragma unroll
+            for (int k = 0; k < U; k++) v[k] = ld_stream_f4(K + i + k * G);
+#pragma unroll
+            for (int k = 0; k < U; k++) {
+                m0 = max(m0, absbits(v[k].x));
+                m1 = max(m1, absbits(v[k].y));
+                m2 = max(m2, absbits(v[k].z));
+                m3 = max(m3, absbits(v[k].w));
+            }
+        }
+        for (; i < n4; i += G) {
+            const float4 v = ld_stream_f4(K + i);
+            m0 = max(m0, absbits(v.x));
+            m1 = max(m1, absbits(v.y));
+            m2 = max(m2, absbits(v.z));
+            m3 = max(m3, absbits(v.w));
+        }
+        const int64_t c4 = g % cols4;
+        if (m0) atomicMax(&bits[4 * c4 + 0], m0);
+        if (m1) atomicMax(&bits[4 * c4 + 1], m1);
+        if (m2) atomicMax(&bits[4 * c4 + 2], m2);
+        if (m3) atomicMax(&bits[4 * c4 + 3], m3);
+    }
+    // ---- 2. the last CTA exchanges and finalizes
+    __shared__ unsigned last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(pa.ticket, 1u) == gridDim.x - 1 ? 1u : 0u;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();  // every CTA's atomics on `bits` are visible
+    const int64_t D = pa.D;
+    const int par = (int)(pa.epoch & 1);
+    const int64_t my_slot = kHdrU32 + ((int64_t)par * pa.nranks + pa.rank) * pa.slot_stride;
+    // 16-byte accesses (D % 4 == 0; slots are 256-byte aligned), independent iterations
+    const int64_t D4 = D / 4;
+    for (int64_t i = threadIdx.x; i < D4; i += kThreads) {
+        const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(bits) + i);
+        for (int r = 0; r < pa.nranks; r++)
+            reinterpret_cast<uint4 *>(pa.bufs[r] + my_slot)[i] = v;  // P2P stores (own buffer for r == rank)
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();  // the slot stores are visible to every GPU before the flags
+        for (int r = 0; r < pa.nranks; r++)
+            st_release_sys(reinterpret_cast<uint64_t *>(pa.bufs[r]) + pa.rank, pa.epoch);
+        *pa.ticket = 0u;  // ready for the next call (stream order separates the launches)
+    }
+    const uint64_t *flags = reinterpret_cast<const uint64_t *>(pa.bufs[pa.rank]);
+    if ((int)threadIdx.x < pa.nranks)
+        while (ld_acquire_sys(flags + threadIdx.x) < pa.epoch) __nanosleep(64);
+    __syncthreads();
+    __threadfence_system();
+    const uint32_t *own = pa.bufs[pa.rank] + kHdrU32 + (int64_t)par * pa.nranks * pa.slot_stride;
+    float4 *scales4 = reinterpret_cast<float4 *>(bits);
+    for (int64_t i = threadIdx.x; i < D4; i += kThreads) {
+        uint4 m = make_uint4(0u, 0u, 0u, 0u);
+        for (int r = 0; r < pa.nranks; r++) {
+            const uint4 v = __ldcv(reinterpret_cast<const uint4 *>(own + (int64_t)r * pa.slot_stride) + i);
+            m.x = max(m.x, v.x);
+            m.y = max(m.y, v.y);
+            m.z = max(m.z, v.z);
+            m.w = max(m.w, v.w);
+        }
+        // Eq. 5/6, reading Q3: IEEE division
+        scales4[i] = make_float4(__fdiv_rn(__uint_as_float(m.x), pa.divisor), __fdiv_rn(__uint_as_float(m.y), pa.divisor),
+                                 __fdiv_rn(__uint_as_float(m.z), pa.divisor), __fdiv_rn(__uint_as_float(m.w), pa.divisor));
+    }
+}
+
+static int64_t slot_stride(int64_t D) { return (D + 63) / 64 * 64; }
+static size_t peer_bytes(int64_t D, int nranks) {
+    return (size_t)(kHdrU32 + 2 * (int64_t)nranks * slot_stride(D)) * 4;
+}
+
+}  // namespace kvq
+
+using namespace kvq;
+
+#define KVQ_REQUIRE(cond, msg)                                    \
+    do {                                                          \
+        if (!(cond)) return fail(KVQ_ERR_INVALID_VALUE, msg);     \
+    } while (0)
+#define KVQ_TRY(expr)                  \
+    do {                               \
+        kvq_status _st = (expr);       \
+        if (_st != KVQ_OK) return _st; \
+    } while (0)
+
+static kvq_status cuda_check(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) return fail(KVQ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return KVQ_OK;
+}
+
+extern "C" size_t kvq_peer_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+extern "C" kvq_status kvq_peer_init(kvq_peer_t *out, int nranks, int rank, int64_t D, void *handle_out) {
+    KVQ_REQUIRE(out && handle_out, "kvq_peer_init: NULL pointer");
+    KVQ_REQUIRE(nranks >= 1 && nranks <= kPeerMax && rank >= 0 && rank < nranks,
+                "kvq_peer_init: need 1 <= nranks <= 16 and 0 <= rank < nranks");
+    KVQ_REQUIRE(D >= 1 && D <= (int64_t(1) << 31), "kvq_peer_init: need 1 <= D <= 2^31");
+    *out = nullptr;
+    KVQ_TRY(device_ok());
+    auto *p = new kvq_peer_s();
+    p->nranks = nranks;
+    p->rank = rank;
+    p->D = D;
+    p->epoch = 0;
+    p->open = false;
+    cudaGetDevice(&p->device);
+    const size_t bytes = peer_bytes(D, nranks);
+    if (cudaMalloc(&p->local, bytes) != cudaSuccess || cudaMemset(p->local, 0, bytes) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
+        if (p->local) cudaFree(p->local);
+        delete p;
+        cudaGetLastError();
+        return fail(KVQ_ERR_CUDA, "kvq_peer_init: exchange buffer allocation failed");
+    }
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, p->local) != cudaSuccess) {
+        cudaFree(p->local);
+        delete p;
+        cudaGetLastError();
+        return fail(KVQ_ERR_CUDA, "kvq_peer_init: cudaIpcGetMemHandle failed");
+    }
+    std::memcpy(handle_out, &h, sizeof(h));
+    *out = p;
+    return KVQ_OK;
+}
+
+extern "C" kvq_status kvq_peer_open(kvq_peer_t p, const void *handles) {
+    KVQ_REQUIRE(p && handles, "kvq_peer_open: NULL pointer");
+    KVQ_REQUIRE(!p->open, "kvq_peer_open: already open");
+    for (int r = 0; r < p->nranks; r++) {
+        if (r == p->rank) {
+            p->bufs[r] = p->local;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const char *>(handles) + (size_t)r * sizeof(h), sizeof(h));
+        void *ptr = nullptr;
+        if (cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            const std::string e = cudaGetErrorString(cudaGetLastError());
+            for (int q = 0; q < r; q++)
+                if (p->mapped[q]) cudaIpcCloseMemHandle(p->mapped[q]), p->mapped[q] = nullptr;
+            return fail(KVQ_ERR_CUDA, "kvq_peer_open: cudaIpcOpenMemHandle(rank " + std::to_string(r) + "): " + e);
+        }
+        p->mapped[r] = p->bufs[r] = static_cast<uint32_t *>(ptr);
+    }
+    p->open = true;
+    return KVQ_OK;
+}
+
+extern "C" kvq_status kvq_peer_destroy(kvq_peer_t p) {
+    if (!p) return KVQ_OK;
+    cudaDeviceSynchronize();
+    for (int r = 0; r < p->nranks; r++)
+        if (p->mapped[r]) cudaIpcCloseMemHandle(p->mapped[r]);
+    cudaFree(p->local);
+    cudaGetLastError();
+    delete p;
+    return KVQ_OK;
+}
+
+extern "C" kvq_status kvq_compute_scales_peer(const float *K, int64_t T, int64_t D, float *scales, kvq_peer_t p,
+                                              void *stream) {
+    KVQ_REQUIRE((K || T == 0) && scales && p, "kvq_compute_scales_peer: NULL pointer");
+    KVQ_REQUIRE(p->open, "kvq_compute_scales_peer: call kvq_peer_open first");
+    KVQ_REQUIRE(D == p->D, "kvq_compute_scales_peer: D differs from kvq_peer_init");
+    KVQ_REQUIRE(T >= 0 && (T == 0 || T <= (int64_t(1) << 62) / D), "kvq_compute_scales_peer: need 0 <= T, T*D <= 2^62");
+    KVQ_REQUIRE(D % 4 == 0 && reinterpret_cast<uintptr_t>(K) % 16 == 0 &&
+                    reinterpret_cast<uintptr_t>(scales) % 16 == 0,
+                "kvq_compute_scales_peer: needs D % 4 == 0 and 16-byte aligned K, scales");
+    KVQ_TRY(device_ok());
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t *bits = reinterpret_cast<uint32_t *>(scales);
+    KVQ_TRY(cuda_check(cudaMemsetAsync(bits, 0, (size_t)D * 4, s), "memset scales"));
+    PeerArgs pa{};
+    for (int r = 0; r < p->nranks; r++) pa.bufs[r] = p->bufs[r];
+    pa.ticket = p->local + kFlagsU32;
+    pa.nranks = p->nranks;
+    pa.rank = p->rank;
+    pa.D = D;
+    pa.slot_stride = slot_stride(D);
+    pa.epoch = ++p->epoch;
+    pa.divisor = 127.0f;
+    const int64_t cols4 = D / 4, n4 = T * cols4;
+    // an empty shard still takes part in the exchange: one CTA with no rows
+    // one full wave of resident CTAs (the streaming loop is sized like colmax_v4_kernel's)
+    static const int resident = [] {
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, colmax_peer_kernel<8>, kThreads, 0) != cudaSuccess ||
+            nb < 1) {
+            cudaGetLastError();
+            nb = 1;
+        }
+        return nb * kThreads;
+    }();
+    StreamPlan plan = n4 > 0 ? plan_stream(T, cols4, resident) : StreamPlan{0, 1};
+    if (plan.blocks < 1) plan.blocks = 1;
+    colmax_peer_kernel<8><<<plan.blocks, kThreads, 0, s>>>(reinterpret_cast<const float4 *>(K), n4, cols4, plan.G,
+                                                           bits, pa);
+    return check_launch("colmax_peer");
+}

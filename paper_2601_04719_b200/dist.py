@@ -53,3 +53,15 @@ def make_comm(rank: int, world: int):
     uid = kvq_comm_unique_id() if rank == 0 else None
     uid = broadcast_bytes(uid, src=0)
     return Comm(uid, world, rank)
+
+
+def make_peer(rank: int, world: int, D: int):
+    """Create the library's peer-memory exchange (kvq_compute_scales_peer): every rank allocates
+    its buffer, the default process group all-gathers the CUDA IPC handles, every rank maps the
+    others'."""
+    from .kvq import Peer
+    p = Peer(world, rank, D)
+    handles = [None] * world
+    dist.all_gather_object(handles, p.ipc_handle)
+    p.open(handles)
+    return p

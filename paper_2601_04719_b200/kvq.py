@@ -94,6 +94,51 @@ class Comm:
             pass
 
 
+class Peer:
+    """Owns a kvq_peer_t: this rank's exchange buffer for kvq_compute_scales_peer (a1 + a7 + a2 in
+    one kernel over peer memory).  Construct on every rank, all-gather ``handle`` (bytes), then
+    call ``open(handles)`` with the handles in rank order."""
+
+    def __init__(self, nranks: int, rank: int, D: int):
+        lib = load()
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(lib.kvq_peer_handle_bytes())
+        check(lib.kvq_peer_init(ctypes.byref(h), nranks, rank, D, buf), "kvq_peer_init")
+        self.handle, self.nranks, self.rank, self.D = h, nranks, rank, D
+        self.ipc_handle = buf.raw
+
+    def open(self, handles) -> None:
+        hb = load().kvq_peer_handle_bytes()
+        assert len(handles) == self.nranks and all(len(x) == hb for x in handles)
+        blob = ctypes.create_string_buffer(b"".join(handles), hb * self.nranks)
+        check(load().kvq_peer_open(self.handle, blob), "kvq_peer_open")
+
+    def destroy(self):
+        if self.handle:
+            check(load().kvq_peer_destroy(self.handle), "kvq_peer_destroy")
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def kvq_compute_scales_peer(K: torch.Tensor, peer: Peer, scales: Optional[torch.Tensor] = None,
+                            stream=None) -> torch.Tensor:
+    """Global scales of a token-sharded K through peer memory (no NCCL); K may have 0 rows."""
+    if K.dim() != 2 or K.dtype != torch.float32 or not K.is_cuda or not K.is_contiguous():
+        raise ValueError("K must be a contiguous float32 CUDA matrix")
+    T, D = K.shape
+    if scales is None:
+        scales = torch.empty(D, dtype=torch.float32, device=K.device)
+    _vec(scales, D, "scales")
+    check(load().kvq_compute_scales_peer(_ptr(K) if T else None, T, D, _ptr(scales), peer.handle,
+                                         _stream(stream)), "kvq_compute_scales_peer")
+    return scales
+
+
 # ----------------------------------------------------------------------------- the hot path
 def kvq_compute_scales(K: torch.Tensor, scales: Optional[torch.Tensor] = None, comm: Optional[Comm] = None,
                        stream=None) -> torch.Tensor:
