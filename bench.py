@@ -189,25 +189,25 @@ def run_kvq(args, cfg, rank, world, local_rank):
     row0, rows = shard_rows(T, world, rank)
     # Under torchrun (even with one process) the NCCL exchange path is exercised:
     # kvq_compute_scales all-reduces the column maxima, the metrics their partials.
-    comm = make_comm(rank, world) if dist.is_available() and dist.is_initialized() else None
-    # a7 (the scale all-reduce MAX): "peer" = kvq_compute_scales_peer, column max + exchange over
-    # CUDA-IPC peer memory + finalize in ONE kernel; "nccl" = column-max kernel, ncclAllReduce(MAX),
-    # finalize kernel.  (Without torchrun there is nothing to exchange: kvq_compute_scales.)
-    peer = None
-    a7 = "none" if comm is None else args.a7
-    if a7 == "peer" and args.format == "int8":
-        try:
-            peer = make_peer(rank, world, cfg["D"])
-        except Exception as e:  # e.g. no peer access between the GPUs: keep the NCCL exchange
-            a7 = f"nccl (peer setup failed: {str(e)[:80]})"
-    elif a7 == "peer":
-        a7 = "nccl (peer path is int8 only)"
+    # The step's collectives (a7: the scale all-reduce MAX; the metric SUM/MAX): "peer" = a communicator
+    # over CUDA-IPC peer memory (kvq_comm_from_peer: column max + exchange + finalize in ONE kernel, the
+    # metric partials exchanged by one small kernel; no NCCL), "nccl" = NCCL all-reduces between the
+    # kernels.  Without torchrun there is nothing to exchange.
+    comm, peer, comm_kind = None, None, None
+    if dist.is_available() and dist.is_initialized():
+        if args.comm == "peer":
+            try:
+                peer = make_peer(rank, world, cfg["D"])
+                comm = kvq.Comm.from_peer(peer)
+                comm_kind = "peer (CUDA-IPC peer memory, libkvq kvq_comm_from_peer; no NCCL)"
+            except Exception as e:  # e.g. no peer access between the GPUs: NCCL instead
+                comm_kind = f"nccl (peer setup failed: {str(e)[:80]})"
+        if comm is None:
+            comm = make_comm(rank, world)
+            comm_kind = comm_kind or "nccl (libkvq kvq_comm_t)"
 
     def compute_scales():
-        if peer is not None:
-            kvq.kvq_compute_scales_peer(K, peer, scales, stream=stream)
-        else:
-            kvq.kvq_compute_scales(K, scales, comm=comm, stream=stream)
+        kvq.kvq_compute_scales(K, scales, comm=comm, stream=stream)
     stream = torch.cuda.current_stream()
 
     # device-resident inputs (generated on the GPU by the seeded counter RNG; rank r makes its rows)
@@ -372,12 +372,12 @@ def run_kvq(args, cfg, rank, world, local_rank):
                "api": "kvq_roundtrip_host_async x2 streams (pinned host K/Q -> scales, codes, metrics)",
                "attn_mean_abs": m_last["attn_mean_abs"]}
 
-    if peer is not None:
+    if comm is not None:
         torch.cuda.synchronize()
         dist.barrier()
-        peer.destroy()
-    if comm is not None:
         comm.destroy()
+    if peer is not None:
+        peer.destroy()
     if rank != 0:
         return
     value = T * D / (ms * 1e-3)
@@ -416,12 +416,13 @@ def run_kvq(args, cfg, rank, world, local_rank):
                    "pipeline": args.pipeline, "format": args.format,
                    "l2_flush": "none needed: inputs larger than L2 (K alone is %.2f GB > 126 MB)" % (4 * T * D / 1e9)
                    if 4 * T * D > 2 * 126e6 else "inputs L2-resident (warm)",
-                   "parallelism": f"token-shard x{world}", "comm": "nccl (libkvq kvq_comm_t)" if comm else None, "a7": a7},
+                   "parallelism": f"token-shard x{world}", "comm": comm_kind},
         "hbm": {"GBps": algo_bytes / (ms * 1e-3) / 1e9 / world, "algo_bytes_per_elem": algo_per_elem,
                 "frac_of_peak_per_gpu": algo_bytes / (ms * 1e-3) / 1e9 / world / pk["hbm_gbs"]},
         "passes": pass_report, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": ((7 if args.format != "int8" else 7 if args.pipeline == "fused" else 8)
-                         - (1 if peer is not None else 0)) * args.steps, "clocks": clk.summary(wall0, wall1),
+        # (a peer communicator replaces the finalize kernel by the fused exchange and adds one metric-exchange
+        # kernel: the count is the same; NCCL's kernels are not counted)
+        "gpu_launches": (7 if args.format != "int8" else 7 if args.pipeline == "fused" else 8) * args.steps, "clocks": clk.summary(wall0, wall1),
         "fidelity": {k: metrics[k] for k in ("l2", "max_abs", "attn_mean_abs", "theoretical_max")},
     }
     print(json.dumps(line), flush=True)
@@ -438,9 +439,9 @@ def main():
     ap.add_argument("--format", default="int8", choices=["int8", "e4m3", "int4", "int2"],
                     help="int8 = the paper's method (headline); e4m3 = the FP8 variant (NEXT-1); "
                          "int4 / int2 = the packed low-bit variants (NEXT-3)")
-    ap.add_argument("--a7", default="peer", choices=["peer", "nccl"],
-                    help="scale all-reduce under torchrun: peer = one fused kernel over CUDA-IPC peer memory "
-                         "(kvq_compute_scales_peer), nccl = ncclAllReduce between the column-max and finalize kernels")
+    ap.add_argument("--comm", default="peer", choices=["peer", "nccl"],
+                    help="collectives under torchrun: peer = CUDA-IPC peer memory (a7 fused into the column-max "
+                         "kernel, metric partials by one exchange kernel; no NCCL), nccl = NCCL all-reduces")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=6)

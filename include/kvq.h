@@ -205,6 +205,13 @@ kvq_status kvq_quantize_fused(const float *K, int64_t T, int64_t D, float *scale
  * concurrently (the last CTA waits for its peers).  kvq_peer_destroy: after all ranks'
  * last call has completed (collective, like ncclCommDestroy). */
 size_t kvq_peer_handle_bytes(void);
+/* A communicator whose collectives (the a7 MAX in kvq_compute_scales[_fmt] -- fused into
+ * the column-max kernel when D % 4 == 0 and K / scales are 16-byte aligned --, the metric
+ * SUM/MAX of kvq_error_metrics / kvq_roundtrip, the running-max MAX of kvq_append and the
+ * host pipeline) all go through the peer's memory instead of NCCL.  The fp64 metric sums
+ * are added in rank order (deterministic, identical on every rank).  `p` stays owned by
+ * the caller and must outlive the communicator (kvq_comm_destroy first). */
+kvq_status kvq_comm_from_peer(kvq_comm_t *out, kvq_peer_t p);
 kvq_status kvq_peer_init(kvq_peer_t *out, int nranks, int rank, int64_t D, void *handle_out);
 kvq_status kvq_peer_open(kvq_peer_t p, const void *handles);
 kvq_status kvq_peer_destroy(kvq_peer_t p);

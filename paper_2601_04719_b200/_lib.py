@@ -68,6 +68,7 @@ SIGNATURES = {
     "kvq_roundtrip_host_async": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
     "kvq_synth_fill": (_int, [_vp, _i64, _i64, _i64, _u64, _int, _vp]),
     "kvq_peer_handle_bytes": (_sz, []),
+    "kvq_comm_from_peer": (_int, [ctypes.POINTER(_vp), _vp]),
     "kvq_peer_init": (_int, [ctypes.POINTER(_vp), _int, _int, _i64, _vp]),
     "kvq_peer_open": (_int, [_vp, _vp]),
     "kvq_peer_destroy": (_int, [_vp]),

@@ -139,10 +139,15 @@ extern "C" kvq_status kvq_compute_scales_fmt(const float *K, int64_t T, int64_t 
     KVQ_TRY(device_ok());
     cudaStream_t s = (cudaStream_t)stream;
     uint32_t *bits = reinterpret_cast<uint32_t *>(scales);
+    const float divisor = fmt == KVQ_FMT_E4M3 ? 448.0f : fmt == KVQ_FMT_INT4 ? 7.0f : fmt == KVQ_FMT_INT2 ? 1.0f : 127.0f;
+    if (kvq_peer_t p = comm_peer(comm)) {
+        // peer-backed communicator: column max + exchange + finalize in one kernel when aligned
+        const kvq_status st = peer_compute_scales(K, T, D, scales, divisor, p, s);
+        if (st != KVQ_ERR_UNSUPPORTED) return st;
+    }
     KVQ_TRY(cuda_check(cudaMemsetAsync(bits, 0, (size_t)D * 4, s), "memset scales"));
     KVQ_TRY(launch_colmax(K, T, D, bits, s));
     if (comm) KVQ_TRY(comm_allreduce_max_u32(comm, bits, (size_t)D, s));
-    const float divisor = fmt == KVQ_FMT_E4M3 ? 448.0f : fmt == KVQ_FMT_INT4 ? 7.0f : fmt == KVQ_FMT_INT2 ? 1.0f : 127.0f;
     return launch_finalize(bits, D, s, divisor);
 }
 

@@ -18,9 +18,10 @@
 #include "kvq_internal.h"
 
 struct kvq_comm_s {
-    ncclComm_t comm;
+    ncclComm_t comm;   // nullptr for a peer-backed communicator
     int nranks;
     int rank;
+    kvq_peer_t peer;   // kvq_comm_from_peer: every collective goes through peer memory (peer.cu), no NCCL
 };
 
 namespace kvq {
@@ -85,7 +86,10 @@ kvq_status allreduce(kvq_comm_t comm, void *buf, size_t count, ncclDataType_t ty
 
 }  // namespace
 
+kvq_peer_t comm_peer(kvq_comm_t comm) { return comm ? comm->peer : nullptr; }
+
 kvq_status comm_allreduce_max_u32(kvq_comm_t comm, uint32_t *buf, size_t count, cudaStream_t s) {
+    if (comm->peer) return peer_allreduce_max_u32(comm->peer, buf, count, s);
     return allreduce(comm, buf, count, ncclUint32, ncclMax, s, "allreduce(max,u32)");
 }
 kvq_status comm_allreduce_sum_f64(kvq_comm_t comm, double *buf, size_t count, cudaStream_t s) {
@@ -98,6 +102,7 @@ kvq_status comm_allreduce_max_u64(kvq_comm_t comm, uint64_t *buf, size_t count, 
 // in ONE NCCL group, i.e. one fused launch instead of two per step.
 kvq_status comm_allreduce_metrics(kvq_comm_t comm, double *sums, size_t nsum, uint64_t *maxes, size_t nmax,
                                   cudaStream_t s) {
+    if (comm->peer) return peer_allreduce_metrics(comm->peer, sums, nsum, maxes, nmax, s);
     NcclApi &a = api();
     if (!a.ok) return fail(KVQ_ERR_NCCL, a.err);
     ncclResult_t r = a.groupStart();
@@ -134,7 +139,7 @@ extern "C" kvq_status kvq_comm_init(kvq_comm_t *out, const void *id128, int nran
     if (!a.ok) return fail(KVQ_ERR_NCCL, a.err);
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof(id));
-    kvq_comm_s *c = new kvq_comm_s{nullptr, nranks, rank};
+    kvq_comm_s *c = new kvq_comm_s{nullptr, nranks, rank, nullptr};
     ncclResult_t r = a.commInitRank(&c->comm, nranks, id, rank);
     if (r != ncclSuccess) {
         delete c;
@@ -144,9 +149,21 @@ extern "C" kvq_status kvq_comm_init(kvq_comm_t *out, const void *id128, int nran
     return KVQ_OK;
 }
 
+extern "C" kvq_status kvq_comm_from_peer(kvq_comm_t *out, kvq_peer_t p) {
+    using namespace kvq;
+    if (!out || !p) return fail(KVQ_ERR_INVALID_VALUE, "kvq_comm_from_peer: NULL");
+    if (!peer_ready(p)) return fail(KVQ_ERR_INVALID_VALUE, "kvq_comm_from_peer: call kvq_peer_open first");
+    *out = new kvq_comm_s{nullptr, peer_nranks(p), peer_rank(p), p};
+    return KVQ_OK;
+}
+
 extern "C" kvq_status kvq_comm_destroy(kvq_comm_t comm) {
     using namespace kvq;
     if (!comm) return KVQ_OK;
+    if (comm->peer) {  // the peer itself belongs to the caller (kvq_peer_destroy)
+        delete comm;
+        return KVQ_OK;
+    }
     NcclApi &a = api();
     kvq_status st = KVQ_OK;
     if (a.ok) {

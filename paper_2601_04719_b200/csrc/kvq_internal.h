@@ -104,6 +104,16 @@ kvq_status launch_scores_codes(const float *Q, int64_t nq, const int8_t *Kq, con
                                int64_t D, float *S, void *ws, size_t ws_bytes, cudaStream_t s);
 
 // ---- comm (comm.cpp)
+// peer-memory exchanges (peer.cu); a kvq_comm_t made with kvq_comm_from_peer routes its collectives here
+int peer_nranks(kvq_peer_t p);
+int peer_rank(kvq_peer_t p);
+bool peer_ready(kvq_peer_t p);
+kvq_status peer_allreduce_max_u32(kvq_peer_t p, uint32_t *buf, size_t count, cudaStream_t s);
+kvq_status peer_allreduce_metrics(kvq_peer_t p, double *sums, size_t nsum, uint64_t *maxes, size_t nmax,
+                                  cudaStream_t s);
+kvq_status peer_compute_scales(const float *K, int64_t T, int64_t D, float *scales, float divisor, kvq_peer_t p,
+                               cudaStream_t s);
+kvq_peer_t comm_peer(kvq_comm_t comm);  // the peer behind a peer-backed communicator, else nullptr
 kvq_status comm_allreduce_max_u32(kvq_comm_t comm, uint32_t *buf, size_t count, cudaStream_t s);
 kvq_status comm_allreduce_sum_f64(kvq_comm_t comm, double *buf, size_t count, cudaStream_t s);
 kvq_status comm_allreduce_max_u64(kvq_comm_t comm, uint64_t *buf, size_t count, cudaStream_t s);

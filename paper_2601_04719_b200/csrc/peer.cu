@@ -44,8 +44,12 @@ struct PeerArgs {
     float divisor;
 };
 
-// exchange buffer layout (u32 units): [flags: kPeerMax x u64 = 32 u32][ticket: 1 u32, pad to 64][slots: 2 x R x S]
-constexpr int64_t kFlagsU32 = 2 * kPeerMax, kHdrU32 = 64;
+// exchange buffer layout (u32 units): [flags: kPeerMax x u64 = 32 u32][ticket: 1 u32, pad to 64]
+// [metric slots: 2 parities x kPeerMax x 8 u64 = 512 u32][column slots: 2 parities x R x S u32]
+// One epoch counter and one flag per rank serve both kinds of exchange: every rank performs the same sequence
+// of exchanges, so epoch e means the same exchange everywhere.
+constexpr int64_t kFlagsU32 = 2 * kPeerMax, kMetU32 = 64, kMetSlotU64 = 8,
+                  kHdrU32 = kMetU32 + 2 * kPeerMax * kMetSlotU64 * 2;
 
 struct kvq_peer_s {
     int nranks, rank, device;
@@ -68,14 +72,85 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
     return v;
 }
 
+// The calling CTA's slot stores are done (before a __syncthreads): publish epoch `pa.epoch` in every rank's
+// buffer, then wait until every rank has published it in ours.  Release/acquire at system scope.
+// (fence.acq_rel.sys, not the sequentially consistent fence.sc.sys of __threadfence_system: the release store
+// is cumulative over the CTA's slot stores ordered before it by bar.sync.)
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void peer_signal_wait(const PeerArgs &pa) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        fence_acq_rel_sys();  // the slot stores are visible to every GPU before the flags
+        for (int r = 0; r < pa.nranks; r++)
+            st_release_sys(reinterpret_cast<uint64_t *>(pa.bufs[r]) + pa.rank, pa.epoch);
+    }
+    const uint64_t *flags = reinterpret_cast<const uint64_t *>(pa.bufs[pa.rank]);
+    if ((int)threadIdx.x < pa.nranks)
+        while (ld_acquire_sys(flags + threadIdx.x) < pa.epoch) __nanosleep(32);
+    __syncthreads();
+    fence_acq_rel_sys();
+}
+
+// All-reduce MAX of `count` (<= D) u32 in place, one CTA.
+__global__ void __launch_bounds__(kThreads) peer_max_u32_kernel(uint32_t *buf, int64_t count,
+                                                                const __grid_constant__ PeerArgs pa) {
+    const int par = (int)(pa.epoch & 1);
+    const int64_t base = kHdrU32 + (int64_t)par * pa.nranks * pa.slot_stride;
+    for (int64_t i = threadIdx.x; i < count; i += kThreads) {
+        const uint32_t v = buf[i];
+        for (int r = 0; r < pa.nranks; r++) pa.bufs[r][base + (int64_t)pa.rank * pa.slot_stride + i] = v;
+    }
+    peer_signal_wait(pa);
+    const uint32_t *own = pa.bufs[pa.rank] + base;
+    for (int64_t i = threadIdx.x; i < count; i += kThreads) {
+        uint32_t m = 0;
+        for (int r = 0; r < pa.nranks; r++) m = max(m, __ldcv(own + (int64_t)r * pa.slot_stride + i));
+        buf[i] = m;
+    }
+}
+
+// The metric partials: nsum fp64 sums (added in rank order: deterministic and identical on every rank) and nmax
+// u64 bit-pattern maxima, in place, one CTA.
+__global__ void peer_metrics_kernel(double *sums, int nsum, uint64_t *maxes, int nmax,
+                                    const __grid_constant__ PeerArgs pa) {
+    const int par = (int)(pa.epoch & 1);
+    const int64_t base = kMetU32 + (int64_t)par * kPeerMax * kMetSlotU64 * 2;  // u32 units
+    const int t = threadIdx.x;
+    if (t < nsum + nmax) {
+        const uint64_t v = t < nsum ? (uint64_t)__double_as_longlong(sums[t]) : maxes[t - nsum];
+        for (int r = 0; r < pa.nranks; r++)
+            reinterpret_cast<uint64_t *>(pa.bufs[r] + base)[pa.rank * kMetSlotU64 + t] = v;
+    }
+    peer_signal_wait(pa);
+    const uint64_t *own = reinterpret_cast<const uint64_t *>(pa.bufs[pa.rank] + base);
+    if (t < nsum) {
+        double acc = 0.0;
+        for (int r = 0; r < pa.nranks; r++) acc += __longlong_as_double((long long)__ldcv(own + r * kMetSlotU64 + t));
+        sums[t] = acc;
+    } else if (t < nsum + nmax) {
+        uint64_t m = 0;
+        for (int r = 0; r < pa.nranks; r++) m = max(m, __ldcv(own + r * kMetSlotU64 + t));
+        maxes[t - nsum] = m;
+    }
+}
+
 template <int U>
 __global__ void __launch_bounds__(kThreads, 6) colmax_peer_kernel(const float4 *__restrict__ K, int64_t n4,
                                                                int64_t cols4, int64_t G, uint32_t *bits,
                                                                const __grid_constant__ PeerArgs pa) {
-    // ---- 1. local column max of this rank's shard (as colmax_v4_kernel, without the smem stage)
+    // ---- 1. local column max of this rank's shard (colmax_v4_kernel's loop: a CTA-level smem max first when
+    //         the columns fit, so narrow heads do not funnel every thread's atomics into D addresses)
+    extern __shared__ uint32_t smax[];  // [4 * cols4] when cols4 <= kThreads
+    const bool share = cols4 <= kThreads;
     const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (share) {
+        for (int i = threadIdx.x; i < 4 * cols4; i += kThreads) smax[i] = 0u;
+        __syncthreads();
+    }
+    uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+    int64_t c4 = 0;
     if (g < G) {
-        uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+        c4 = g % cols4;
         int64_t i = g;
         for (; i + (U - 1) * G < n4; i += U * G) {
             float4 v[U];
@@ -96,7 +171,18 @@ __global__ void __launch_bounds__(kThreads, 6) colmax_peer_kernel(const float4 *
             m2 = max(m2, absbits(v.z));
             m3 = max(m3, absbits(v.w));
         }
-        const int64_t c4 = g % cols4;
+    }
+    if (share) {
+        if (g < G) {
+            atomicMax(&smax[4 * c4 + 0], m0);
+            atomicMax(&smax[4 * c4 + 1], m1);
+            atomicMax(&smax[4 * c4 + 2], m2);
+            atomicMax(&smax[4 * c4 + 3], m3);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < 4 * cols4; i += kThreads)
+            if (smax[i]) atomicMax(&bits[i], smax[i]);
+    } else if (g < G) {
         if (m0) atomicMax(&bits[4 * c4 + 0], m0);
         if (m1) atomicMax(&bits[4 * c4 + 1], m1);
         if (m2) atomicMax(&bits[4 * c4 + 2], m2);
@@ -120,18 +206,8 @@ __global__ void __launch_bounds__(kThreads, 6) colmax_peer_kernel(const float4 *
         for (int r = 0; r < pa.nranks; r++)
             reinterpret_cast<uint4 *>(pa.bufs[r] + my_slot)[i] = v;  // P2P stores (own buffer for r == rank)
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();  // the slot stores are visible to every GPU before the flags
-        for (int r = 0; r < pa.nranks; r++)
-            st_release_sys(reinterpret_cast<uint64_t *>(pa.bufs[r]) + pa.rank, pa.epoch);
-        *pa.ticket = 0u;  // ready for the next call (stream order separates the launches)
-    }
-    const uint64_t *flags = reinterpret_cast<const uint64_t *>(pa.bufs[pa.rank]);
-    if ((int)threadIdx.x < pa.nranks)
-        while (ld_acquire_sys(flags + threadIdx.x) < pa.epoch) __nanosleep(64);
-    __syncthreads();
-    __threadfence_system();
+    if (threadIdx.x == 0) *pa.ticket = 0u;  // ready for the next call (stream order separates the launches)
+    peer_signal_wait(pa);
     const uint32_t *own = pa.bufs[pa.rank] + kHdrU32 + (int64_t)par * pa.nranks * pa.slot_stride;
     float4 *scales4 = reinterpret_cast<float4 *>(bits);
     for (int64_t i = threadIdx.x; i < D4; i += kThreads) {
@@ -168,10 +244,6 @@ using namespace kvq;
         if (_st != KVQ_OK) return _st; \
     } while (0)
 
-static kvq_status cuda_check(cudaError_t e, const char *what) {
-    if (e != cudaSuccess) return fail(KVQ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-    return KVQ_OK;
-}
 
 extern "C" size_t kvq_peer_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
 
@@ -243,6 +315,74 @@ extern "C" kvq_status kvq_peer_destroy(kvq_peer_t p) {
     return KVQ_OK;
 }
 
+static PeerArgs peer_args(kvq_peer_t p, float divisor) {
+    PeerArgs pa{};
+    for (int r = 0; r < p->nranks; r++) pa.bufs[r] = p->bufs[r];
+    pa.ticket = p->local + kFlagsU32;
+    pa.nranks = p->nranks;
+    pa.rank = p->rank;
+    pa.D = p->D;
+    pa.slot_stride = slot_stride(p->D);
+    pa.epoch = ++p->epoch;
+    pa.divisor = divisor;
+    return pa;
+}
+
+namespace kvq {
+
+int peer_nranks(kvq_peer_t p) { return p->nranks; }
+int peer_rank(kvq_peer_t p) { return p->rank; }
+bool peer_ready(kvq_peer_t p) { return p && p->open; }
+
+kvq_status peer_allreduce_max_u32(kvq_peer_t p, uint32_t *buf, size_t count, cudaStream_t s) {
+    if (!peer_ready(p)) return fail(KVQ_ERR_INVALID_VALUE, "peer exchange: kvq_peer_open was not called");
+    if ((int64_t)count > p->D) return fail(KVQ_ERR_INVALID_VALUE, "peer exchange: count exceeds the peer's D");
+    const PeerArgs pa = peer_args(p, 1.0f);
+    peer_max_u32_kernel<<<1, kThreads, 0, s>>>(buf, (int64_t)count, pa);
+    return check_launch("peer_max_u32");
+}
+
+kvq_status peer_allreduce_metrics(kvq_peer_t p, double *sums, size_t nsum, uint64_t *maxes, size_t nmax,
+                                  cudaStream_t s) {
+    if (!peer_ready(p)) return fail(KVQ_ERR_INVALID_VALUE, "peer exchange: kvq_peer_open was not called");
+    if (nsum + nmax > (size_t)kMetSlotU64) return fail(KVQ_ERR_INVALID_VALUE, "peer exchange: too many metrics");
+    const PeerArgs pa = peer_args(p, 1.0f);
+    peer_metrics_kernel<<<1, 32, 0, s>>>(sums, (int)nsum, maxes, (int)nmax, pa);
+    return check_launch("peer_metrics");
+}
+
+// a1 + a7 + a2 in one kernel; KVQ_ERR_UNSUPPORTED when the shape/alignment needs the generic path.
+kvq_status peer_compute_scales(const float *K, int64_t T, int64_t D, float *scales, float divisor, kvq_peer_t p,
+                               cudaStream_t s) {
+    if (!peer_ready(p)) return fail(KVQ_ERR_INVALID_VALUE, "peer exchange: kvq_peer_open was not called");
+    if (D != p->D || D % 4 || reinterpret_cast<uintptr_t>(K) % 16 || reinterpret_cast<uintptr_t>(scales) % 16)
+        return KVQ_ERR_UNSUPPORTED;
+    uint32_t *bits = reinterpret_cast<uint32_t *>(scales);
+    if (cudaMemsetAsync(bits, 0, (size_t)D * 4, s) != cudaSuccess) return check_launch("memset scales");
+    const PeerArgs pa = peer_args(p, divisor);
+    const int64_t cols4 = D / 4, n4 = T * cols4;
+    // one full wave of resident CTAs (the streaming loop is sized like colmax_v4_kernel's)
+    const size_t smem = cols4 <= kThreads ? (size_t)4 * cols4 * sizeof(uint32_t) : 0;
+    static const int resident = [] {
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, colmax_peer_kernel<8>, kThreads,
+                                                          4 * kThreads * sizeof(uint32_t)) != cudaSuccess ||
+            nb < 1) {
+            cudaGetLastError();
+            nb = 1;
+        }
+        return nb * kThreads;
+    }();
+    // an empty shard still takes part in the exchange: one CTA with no rows
+    StreamPlan plan = n4 > 0 ? plan_stream(T, cols4, resident) : StreamPlan{0, 1};
+    if (plan.blocks < 1) plan.blocks = 1;
+    colmax_peer_kernel<8><<<plan.blocks, kThreads, smem, s>>>(reinterpret_cast<const float4 *>(K), n4, cols4, plan.G,
+                                                           bits, pa);
+    return check_launch("colmax_peer");
+}
+
+}  // namespace kvq
+
 extern "C" kvq_status kvq_compute_scales_peer(const float *K, int64_t T, int64_t D, float *scales, kvq_peer_t p,
                                               void *stream) {
     KVQ_REQUIRE((K || T == 0) && scales && p, "kvq_compute_scales_peer: NULL pointer");
@@ -253,33 +393,5 @@ extern "C" kvq_status kvq_compute_scales_peer(const float *K, int64_t T, int64_t
                     reinterpret_cast<uintptr_t>(scales) % 16 == 0,
                 "kvq_compute_scales_peer: needs D % 4 == 0 and 16-byte aligned K, scales");
     KVQ_TRY(device_ok());
-    cudaStream_t s = (cudaStream_t)stream;
-    uint32_t *bits = reinterpret_cast<uint32_t *>(scales);
-    KVQ_TRY(cuda_check(cudaMemsetAsync(bits, 0, (size_t)D * 4, s), "memset scales"));
-    PeerArgs pa{};
-    for (int r = 0; r < p->nranks; r++) pa.bufs[r] = p->bufs[r];
-    pa.ticket = p->local + kFlagsU32;
-    pa.nranks = p->nranks;
-    pa.rank = p->rank;
-    pa.D = D;
-    pa.slot_stride = slot_stride(D);
-    pa.epoch = ++p->epoch;
-    pa.divisor = 127.0f;
-    const int64_t cols4 = D / 4, n4 = T * cols4;
-    // an empty shard still takes part in the exchange: one CTA with no rows
-    // one full wave of resident CTAs (the streaming loop is sized like colmax_v4_kernel's)
-    static const int resident = [] {
-        int nb = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, colmax_peer_kernel<8>, kThreads, 0) != cudaSuccess ||
-            nb < 1) {
-            cudaGetLastError();
-            nb = 1;
-        }
-        return nb * kThreads;
-    }();
-    StreamPlan plan = n4 > 0 ? plan_stream(T, cols4, resident) : StreamPlan{0, 1};
-    if (plan.blocks < 1) plan.blocks = 1;
-    colmax_peer_kernel<8><<<plan.blocks, kThreads, 0, s>>>(reinterpret_cast<const float4 *>(K), n4, cols4, plan.G,
-                                                           bits, pa);
-    return check_launch("colmax_peer");
+    return peer_compute_scales(K, T, D, scales, 127.0f, p, (cudaStream_t)stream);
 }

@@ -82,6 +82,15 @@ class Comm:
         check(load().kvq_comm_init(ctypes.byref(h), idbuf, nranks, rank), "kvq_comm_init")
         self.handle, self.nranks, self.rank = h, nranks, rank
 
+    @classmethod
+    def from_peer(cls, peer: "Peer") -> "Comm":
+        """A communicator whose collectives go through peer memory (kvq_comm_from_peer), no NCCL."""
+        c = cls.__new__(cls)
+        h = ctypes.c_void_p()
+        check(load().kvq_comm_from_peer(ctypes.byref(h), peer.handle), "kvq_comm_from_peer")
+        c.handle, c.nranks, c.rank, c.peer = h, peer.nranks, peer.rank, peer  # keeps the peer alive
+        return c
+
     def destroy(self):
         if self.handle:
             check(load().kvq_comm_destroy(self.handle), "kvq_comm_destroy")

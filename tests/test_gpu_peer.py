@@ -92,6 +92,48 @@ def _rank_main(rank, world, port, out_dir):
             dist.barrier()
             p.destroy()
             dist.barrier()
+        # a peer-backed communicator: every collective of scales (INT8 fused, E4M3 fused, unaligned D generic),
+        # roundtrip and metrics goes through peer memory, no NCCL
+        for T, D, nq in [(700, 256, 64), (333, 64, 17)]:
+            p = make_peer(rank, world, D)
+            comm = kvq.Comm.from_peer(p)
+            row0, rows = shard_rows(T, world, rank)
+            Kfull = orc.fill(T, D, 42, 1)
+            K = kvq.kvq_synth_fill(rows, D, row0=row0, seed=42, dist=1)
+            Q = orc.fill(nq, D, 43)
+            so, qo, kho = orc.roundtrip(Kfull)
+            for it in range(2):
+                s = kvq.kvq_compute_scales(K, comm=comm)
+                if not np.array_equal(host(s).view(np.uint32), so.view(np.uint32)):
+                    msgs.append(f"comm scales T={T} D={D}")
+                Kq, Kh, out = kvq.kvq_roundtrip(K, s, torch.from_numpy(Q).cuda(), comm=comm)
+                m = kvq.metrics_from_device(out)
+                if not (np.array_equal(host(Kq), qo[row0:row0 + rows]) and
+                        np.array_equal(host(Kh).view(np.uint32), kho[row0:row0 + rows].view(np.uint32))):
+                    msgs.append(f"comm roundtrip codes T={T} D={D}")
+                ss, mx = orc.recon_errors(Kfull, kho)
+                attn = orc.attention_error(Q, Kfull, kho)
+                if m["max_abs"] != mx or abs(m["sum_sq"] - ss) > 1e-5 * ss or abs(m["attn_mean_abs"] - attn) > 1e-5 * attn:
+                    msgs.append(f"comm metrics T={T} D={D}: {m} vs {ss} {mx} {attn}")
+                me = kvq.kvq_error_metrics(K, Kh, torch.from_numpy(Q).cuda(), s, comm=comm)
+                if me["max_abs"] != mx or abs(me["attn_mean_abs"] - attn) > 1e-5 * attn:
+                    msgs.append(f"comm error_metrics T={T} D={D}")
+                s8 = kvq.kvq_compute_scales_fmt(K, kvq.FMT_E4M3, comm=comm)
+                if not np.array_equal(host(s8).view(np.uint32), orc.compute_scales_e4m3(Kfull).view(np.uint32)):
+                    msgs.append(f"comm e4m3 scales T={T} D={D}")
+            Ku = kvq.kvq_synth_fill(rows, 13, row0=row0, seed=5)  # D % 4 != 0: colmax + peer MAX kernel + finalize
+            pu = make_peer(rank, world, 13)
+            cu = kvq.Comm.from_peer(pu)
+            su = kvq.kvq_compute_scales(Ku, comm=cu)
+            if not np.array_equal(host(su).view(np.uint32), orc.compute_scales(orc.fill(T, 13, 5)).view(np.uint32)):
+                msgs.append(f"comm unaligned scales T={T}")
+            torch.cuda.synchronize()
+            dist.barrier()
+            comm.destroy()
+            cu.destroy()
+            p.destroy()
+            pu.destroy()
+            dist.barrier()
         dist.destroy_process_group()
         with open(ok_path, "w") as f:
             f.write("OK\n" if not msgs else "\n".join(msgs))
