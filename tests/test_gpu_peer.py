@@ -134,6 +134,32 @@ def _rank_main(rank, world, port, out_dir):
             p.destroy()
             pu.destroy()
             dist.barrier()
+        # token-sharded streaming cache (kvq_append) over the peer communicator: after every append the global
+        # scales and each rank's codes equal the batch method on the union of all ranks' rows so far
+        D = 64
+        p = make_peer(rank, world, D)
+        comm = kvq.Comm.from_peer(p)
+        Kall = orc.fill(300 * world, D, 17, 1)
+        cache = kvq.AppendCache(300, D, keep_khat=True, comm=comm)
+        steps = [(5, 0, 2), (1, 3, 0), (100, 7, 40), (0, 0, 0), (50, 90, 1), (1, 1, 1)]
+        done = [0] * world
+        for st_ in steps:
+            n = st_[rank % 3]
+            rows = torch.from_numpy(Kall[300 * rank + done[rank]:300 * rank + done[rank] + n]).cuda() if n else None
+            cache.append(rows)
+            done = [done[r] + st_[r % 3] for r in range(world)]
+            union = np.concatenate([Kall[300 * r:300 * r + done[r]] for r in range(world)])
+            su = orc.compute_scales(union) if union.shape[0] else np.zeros(D, np.float32)
+            if not np.array_equal(host(cache.scales).view(np.uint32), su.view(np.uint32)):
+                msgs.append(f"append scales after {done}")
+            mine = Kall[300 * rank:300 * rank + done[rank]]
+            if done[rank] and not np.array_equal(host(cache.Kq[:done[rank]]), orc.quantize(mine, su)):
+                msgs.append(f"append codes after {done}")
+        torch.cuda.synchronize()
+        dist.barrier()
+        comm.destroy()
+        p.destroy()
+        dist.barrier()
         dist.destroy_process_group()
         with open(ok_path, "w") as f:
             f.write("OK\n" if not msgs else "\n".join(msgs))
