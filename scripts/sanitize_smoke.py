@@ -39,3 +39,19 @@ for (T, D, nq) in [(300, 64, 7), (129, 48, 64), (77, 13, 5), (1, 4, 1), (257, 10
     cache.append(K[T // 2 + 1: T])
     torch.cuda.synchronize()
     print(T, D, nq, "ok", m["attn_mean_abs"], single)
+# peer-memory collectives at world 1 (the exchange kernels, the fused column max + exchange + finalize)
+for D in (64, 13, 1024):
+    p = kvq.Peer(1, 0, D)
+    p.open([p.ipc_handle])
+    c = kvq.Comm.from_peer(p)
+    K = kvq.kvq_synth_fill(200, D, seed=3, dist=1)
+    Q = kvq.kvq_synth_fill(9, D, seed=43)
+    s = kvq.kvq_compute_scales(K, comm=c)
+    if D % 4 == 0:
+        s2 = kvq.kvq_compute_scales_peer(K, p)
+        assert torch.equal(s, s2)
+    _, kh, out = kvq.kvq_roundtrip(K, s, Q, comm=c)
+    m = kvq.kvq_error_metrics(K, kh, Q, s, comm=c)
+    torch.cuda.synchronize()
+    c.destroy()
+    p.destroy()
