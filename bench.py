@@ -444,7 +444,7 @@ def main():
                          "kernel, metric partials by one exchange kernel; no NCCL), nccl = NCCL all-reduces")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-pass-events", dest="pass_events", action="store_false")
     args = ap.parse_args()
