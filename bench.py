@@ -347,9 +347,20 @@ def run_kvq(args, cfg, rank, world, local_rank):
                               kq=torch.empty((rows, D), dtype=torch.int8).pin_memory(),
                               m=torch.empty(kvq.METRICS_BYTES, dtype=torch.uint8).pin_memory()))
 
+        # One communicator per slot stream: a communicator's exchanges must execute in the same order on every
+        # rank, which two streams sharing one communicator would not guarantee (NCCL's rule as well).
+        extra = []
+        if comm is not None:
+            if peer is not None:
+                p2 = make_peer(rank, world, D)
+                extra = [kvq.Comm.from_peer(p2), p2]
+            else:
+                extra = [make_comm(rank, world)]
+        slots[0]["comm"], slots[1]["comm"] = comm, (extra[0] if extra else None)
+
         def e2e_step(i):
             sl = slots[i % 2]
-            kvq.kvq_roundtrip_host_async(K_host, Q_host, sl["sc"], sl["kq"], sl["m"], sl["ws"], comm=comm,
+            kvq.kvq_roundtrip_host_async(K_host, Q_host, sl["sc"], sl["kq"], sl["m"], sl["ws"], comm=sl["comm"],
                                          stream=sl["stream"])
 
         for i in range(2):  # warm-up (allocations, first-touch of pinned pages)
@@ -371,6 +382,11 @@ def run_kvq(args, cfg, rank, world, local_rank):
                "steps": e2e_steps, "timing": "host wall clock around the pipelined steps (max over ranks)",
                "api": "kvq_roundtrip_host_async x2 streams (pinned host K/Q -> scales, codes, metrics)",
                "attn_mean_abs": m_last["attn_mean_abs"]}
+        if extra:
+            torch.cuda.synchronize()
+            dist.barrier()
+            for x in extra:
+                x.destroy()
 
     if comm is not None:
         torch.cuda.synchronize()

@@ -53,7 +53,10 @@ typedef enum {
  * KVQ_FMT_INT2 the packed low-bit variants (NEXT-3; reading Q19). */
 typedef enum { KVQ_FMT_INT8 = 0, KVQ_FMT_E4M3 = 1, KVQ_FMT_INT4 = 2, KVQ_FMT_INT2 = 3 } kvq_format;
 
-/* Opaque multi-GPU communicator (wraps an ncclComm_t; NULL = single GPU). */
+/* Opaque multi-GPU communicator (wraps an ncclComm_t, or a kvq_peer_t via
+ * kvq_comm_from_peer; NULL = single GPU).  Every rank must issue a communicator's
+ * calls in the same order, and their exchanges must execute in that order: use one
+ * stream per communicator (a second concurrent stream needs its own communicator). */
 typedef struct kvq_comm_s *kvq_comm_t;
 
 /* Opaque peer-memory exchange (library-owned device buffer shared over CUDA IPC). */
