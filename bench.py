@@ -144,6 +144,38 @@ def oracle_step(cfg, rows: int):
     return time.perf_counter() - t0, rows * D
 
 
+def host_info() -> dict:
+    """The host the oracle runs on (CPU model, core count, one core used)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"host_cpu": model, "host_cpu_count": os.cpu_count()}
+
+
+class one_core:
+    """Pin the calling process to one core while the single-threaded oracle is timed."""
+
+    def __enter__(self):
+        self.saved = None
+        if hasattr(os, "sched_getaffinity"):
+            try:
+                self.saved = os.sched_getaffinity(0)
+                os.sched_setaffinity(0, {min(self.saved)})
+            except OSError:
+                self.saved = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.saved is not None:
+            os.sched_setaffinity(0, self.saved)
+
+
 def oracle_rows_for(cfg, seconds: float) -> int:
     t, n = oracle_step(cfg, 8)
     per_row = t / 8
@@ -158,9 +190,10 @@ def run_reference(args, cfg, rank, world):
     for _ in range(args.warmup):
         oracle_step(cfg, rows)
     ts = []
-    for _ in range(args.steps):
-        t, n = oracle_step(cfg, rows)
-        ts.append(t)
+    with one_core():
+        for _ in range(args.steps):
+            t, n = oracle_step(cfg, rows)
+            ts.append(t)
     tot = sum(ts)
     value = rows * cfg["D"] * args.steps / tot
     sample = f"first {rows} rows of {cfg['name']} ({rows}x{cfg['D']} elements) per step, nq={cfg['nq']}"
@@ -169,7 +202,8 @@ def run_reference(args, cfg, rank, world):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (splitmix64 lattice uniform [-1,1), SURVEY §8(d))",
             "config": {"workload": f"{cfg['name']}: {cfg['desc']}", "T": cfg["T"], "D": cfg["D"], "nq": cfg["nq"]},
-            "cpu_baseline": {"value": value, "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": sample,
+                             **host_info()},
             "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -411,12 +445,13 @@ def run_kvq(args, cfg, rank, world, local_rank):
                     "ms_per_launch": t}
     cpu = None
     if world == 1 and not args.no_cpu:
-        rows_cpu = oracle_rows_for(cfg, args.cpu_seconds)
-        t_cpu, n_cpu = oracle_step(cfg, rows_cpu)
+        with one_core():
+            rows_cpu = oracle_rows_for(cfg, args.cpu_seconds)
+            t_cpu, n_cpu = oracle_step(cfg, rows_cpu)
         cpu = {"value": n_cpu / t_cpu, "unit": "elements/s", "cores": 1, "kind": "oracle",
                "sample": f"first {rows_cpu} rows of {cfg['name']} ({n_cpu} elements): scales+quantize+dequantize"
-                         f"+L2/max+attention(nq={nq}), plain C single thread, generation excluded",
-               "seconds": t_cpu}
+                         f"+L2/max+attention(nq={nq}), plain C single thread pinned to one core, generation excluded",
+               "seconds": t_cpu, **host_info()}
     line = {
         "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
