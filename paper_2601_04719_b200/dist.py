@@ -55,13 +55,39 @@ def make_comm(rank: int, world: int):
     return Comm(uid, world, rank)
 
 
+def all_ranks_ok(ok: bool) -> bool:
+    """True iff `ok` on every rank of the default process group (MIN all-reduce)."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return ok
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
+
+
 def make_peer(rank: int, world: int, D: int):
-    """Create the library's peer-memory exchange (kvq_compute_scales_peer): every rank allocates
-    its buffer, the default process group all-gathers the CUDA IPC handles, every rank maps the
-    others'."""
+    """Create the library's peer-memory exchange (kvq_compute_scales_peer / kvq_comm_from_peer):
+    every rank allocates its buffer, the default process group all-gathers the CUDA IPC handles,
+    every rank maps the others'.  Collective: if any rank fails, every rank raises (so all of
+    them can fall back to NCCL together instead of waiting on a peer that never signals)."""
     from .kvq import Peer
-    p = Peer(world, rank, D)
+    p, handle, err = None, b"", None
+    try:
+        p = Peer(world, rank, D)
+        handle = p.ipc_handle
+    except Exception as e:  # noqa: BLE001
+        err = e
     handles = [None] * world
-    dist.all_gather_object(handles, p.ipc_handle)
-    p.open(handles)
+    dist.all_gather_object(handles, handle)
+    if err is None and all(handles):
+        try:
+            p.open(handles)
+        except Exception as e:  # noqa: BLE001
+            err = e
+    elif err is None:
+        err = RuntimeError("kvq peer setup failed on another rank")
+    if not all_ranks_ok(err is None):
+        if p is not None:
+            p.destroy()
+        raise err if err is not None else RuntimeError("kvq peer setup failed on another rank")
     return p

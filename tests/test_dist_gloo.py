@@ -159,3 +159,35 @@ def test_append_sharded_equals_batch(tmp_path):
     assert np.array_equal(s0.view(np.uint32), batch_s.view(np.uint32))
     for r in range(2):
         assert np.array_equal(np.load(tmp_path / f"app_q{r}.npy"), oracle.quantize(Ks[r], batch_s))
+
+
+def _consensus_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_2601_04719_b200.dist import all_ranks_ok, make_peer
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mixed = all_ranks_ok(rank != 1)        # one rank fails -> every rank sees failure
+        agree = all_ranks_ok(True)
+        # peer setup is collective: here (no GPU) it fails on every rank, and every rank must raise
+        # instead of one rank waiting on a peer that never signals
+        try:
+            make_peer(rank, world, 64)
+            raised = False
+        except Exception:  # noqa: BLE001
+            raised = True
+        np.savez(os.path.join(out_dir, f"c{rank}.npz"), mixed=mixed, agree=agree, raised=raised)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure path of the collective setup")
+def test_peer_setup_is_collective(tmp_path):
+    world, port = 3, _free_port()
+    mp.start_processes(_consensus_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    for r in range(world):
+        z = np.load(tmp_path / f"c{r}.npz")
+        assert not bool(z["mixed"]) and bool(z["agree"]) and bool(z["raised"])
