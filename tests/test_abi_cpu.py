@@ -127,3 +127,26 @@ def test_next_rows_validation_without_gpu(lib):
         assert lib.kvq_quantize_packed(A, 2 * A, 4, 8, 4, 3 * A, None, None) != OK
         assert lib.kvq_append(A, 0, 1, 8, 2 * A, 3 * A, 4 * A, None, 5 * A, ws, None, None) != OK
         assert lib.kvq_scores_from_codes(A, 4, 2 * A, 3 * A, 8, 16, 4 * A, None, 0, None) != OK
+
+
+def test_peer_api_validation_without_gpu(lib):
+    """Peer-memory exchange (kvq_peer_*, kvq_comm_from_peer, kvq_compute_scales_peer): synchronous argument
+    checks, and no silent success without a GPU."""
+    import ctypes
+    import torch
+    from paper_2601_04719_b200._lib import ERR_INVALID_VALUE, OK
+    assert lib.kvq_peer_handle_bytes() == 64  # cudaIpcMemHandle_t
+    h = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(64)
+    assert lib.kvq_peer_init(None, 2, 0, 64, buf) == ERR_INVALID_VALUE
+    assert lib.kvq_peer_init(ctypes.byref(h), 0, 0, 64, buf) == ERR_INVALID_VALUE   # nranks
+    assert lib.kvq_peer_init(ctypes.byref(h), 17, 0, 64, buf) == ERR_INVALID_VALUE  # nranks > 16
+    assert lib.kvq_peer_init(ctypes.byref(h), 2, 2, 64, buf) == ERR_INVALID_VALUE   # rank
+    assert lib.kvq_peer_init(ctypes.byref(h), 2, 0, 0, buf) == ERR_INVALID_VALUE    # D
+    assert lib.kvq_peer_init(ctypes.byref(h), 2, 0, 64, None) == ERR_INVALID_VALUE  # handle out
+    assert lib.kvq_peer_open(None, buf) == ERR_INVALID_VALUE
+    assert lib.kvq_comm_from_peer(ctypes.byref(h), None) == ERR_INVALID_VALUE
+    assert lib.kvq_compute_scales_peer(1 << 20, 4, 64, 2 << 20, None, None) == ERR_INVALID_VALUE
+    assert lib.kvq_peer_destroy(None) == OK
+    if not torch.cuda.is_available():
+        assert lib.kvq_peer_init(ctypes.byref(h), 2, 0, 64, buf) != OK
