@@ -34,6 +34,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -49,9 +50,12 @@ constexpr int QST = 4, AST = 4;
 // Input ring: modes 0/1 stage K and K_hat (32 KB) x 4; the fused mode stages K only
 // (16 KB) x 8, i.e. 128 KB in flight per SM either way (Little's law at ~44 GB/s/SM).
 constexpr int KST_MAX = 8;
+#ifndef KVQ_TC_KST01
+#define KVQ_TC_KST01 4  // modes 0/1 ring depth (experiments: -DKVQ_TC_KST01=5 fills the 160 KB buffer)
+#endif
 template <int MODE>
 struct Ring {
-    static constexpr int kst = MODE == 2 ? 8 : 4;
+    static constexpr int kst = MODE == 2 ? 8 : KVQ_TC_KST01;
     static constexpr uint32_t stage = MODE == 2 ? 16384u : 32768u;
 };
 // warps: 0 K producer, 1 MMA (+TMEM alloc), 2 output stores (fused mode), 3 Q producer, 4-11 converters (2 per TMEM lane
@@ -111,7 +115,68 @@ struct TcParams {
     int hints;           // L2 policies: bit0 K loads evict-first, bit1 output stores evict-first (default both;
                          // evict-first loads with normal stores cost ~0.6 GB of extra DRAM reads at C4)
     float *Kh;           // MODE 2: K_hat output [T][D]
+    int ngrp;            // work units (groups of CODE_KB K-blocks) per tile row
+    double *split;       // MODE 0, 2: [grid][2][BN][BM] fp64 Delta of tiles split between CTAs (nullptr: MODE 1)
 };
+
+// Work distribution.  A work unit is one group of CODE_KB K-blocks (one accumulator chunk, one code
+// box) of one 128-row tile; units are numbered tile-major.  Every CTA first takes whole tiles in waves
+// (tile b, b + G, ...: the G CTAs stream G adjacent tiles at a time, the write pattern the HBM measured
+// best), then, in modes 0 and 2, an equal contiguous share (to within one unit) of the units of the
+// R = ntiles mod G tiles left over, so that all SMs stream to the end of the pass (with whole tiles
+// only, 512 tiles on 148 SMs run 4 waves, the last 46% full).  A left-over tile whose units fall to two
+// or more CTAs is "split": each CTA holds its piece's Delta in fp64 and writes it to slot 0 (the piece
+// starts inside the tile) or slot 1 (it starts at the tile's first unit), and split_combine_kernel adds
+// the pieces in CTA order and takes |Delta|.  Mode 1 (scores) keeps whole tiles only.
+struct Units {
+    int n, nfull;              // units of this CTA; whole-tile units among them
+    int tail_tile, tail_grp;   // tile and group of the first unit of the tail share
+    int G, ngrp;
+};
+// Computed once by every thread and broadcast from lane 0 (__shfl_sync), so that the compiler knows
+// the loop state is warp-uniform: the MMA issuer's descriptors then stay in uniform registers (with
+// division results in per-thread registers it re-broadcasts them for every tcgen05.mma).
+__device__ __forceinline__ Units make_units(const TcParams &p) {
+    const int b = blockIdx.x, G = gridDim.x;
+    int n, nfull, tt = 0, tg = 0;
+    if (!p.split) {
+        nfull = n = (p.ntiles - b + G - 1) / G * p.ngrp;
+    } else {
+        const int64_t W = p.ntiles / G, Ut = (int64_t)(p.ntiles % G) * p.ngrp;
+        const int64_t t0 = Ut * b / G, t1 = Ut * (b + 1) / G;
+        nfull = (int)(W * p.ngrp);
+        n = nfull + (int)(t1 - t0);
+        const int64_t tail0 = W * G * p.ngrp + t0;
+        tt = (int)(tail0 / p.ngrp);
+        tg = (int)(tail0 % p.ngrp);
+    }
+    Units us;
+    us.n = __shfl_sync(0xffffffffu, n, 0);
+    us.nfull = __shfl_sync(0xffffffffu, nfull, 0);
+    us.tail_tile = __shfl_sync(0xffffffffu, tt, 0);
+    us.tail_grp = __shfl_sync(0xffffffffu, tg, 0);
+    us.G = G;
+    us.ngrp = p.ngrp;
+    return us;
+}
+// Walks a CTA's units in order (whole-tile waves, then the tail share) without integer division.
+struct UnitWalk {
+    int i, n, nfull, tile, grp, ngrp, G, tail_tile, tail_grp;
+    __device__ __forceinline__ explicit UnitWalk(const Units &u)
+        : i(0), n(u.n), nfull(u.nfull), tile(u.nfull > 0 ? (int)blockIdx.x : u.tail_tile),
+          grp(u.nfull > 0 ? 0 : u.tail_grp), ngrp(u.ngrp), G(u.G), tail_tile(u.tail_tile), tail_grp(u.tail_grp) {}
+    __device__ __forceinline__ bool ok() const { return i < n; }
+    __device__ __forceinline__ void next() {
+        if (++i == nfull) {  // whole-tile waves done: continue at the tail share
+            tile = tail_tile;
+            grp = tail_grp;
+        } else if (++grp == ngrp) {
+            grp = 0;
+            tile += i < nfull ? G : 1;
+        }
+    }
+};
+static_assert(CHUNK_KB == CODE_KB, "one accumulator chunk per work unit");
 
 // Q [nq][D] -> per K-block kb: [hi | lo] tiles of BN x BK tf32 in the canonical
 // K-major SWIZZLE_NONE layout: core matrix (kg = k/4, rg = n/8) at byte
@@ -152,6 +217,50 @@ __global__ void colq_kernel(const float *__restrict__ scales, int64_t D, int64_t
     }
 }
 
+// Split tiles (see make_units): block k < G-1 looks at the boundary between the tail shares of CTAs k
+// and k+1.  If it falls inside a tile and is that tile's first boundary, the block adds the tile's
+// pieces in CTA order (CTA k: slot 1, or slot 0 if its share also started inside the tile; CTAs k+1..:
+// slot 0), takes |Delta| over the tile's rows < T and queries < nq, and writes the sum as partial G + k
+// (zero otherwise).  Fixed order throughout: deterministic.
+constexpr int COMBINE_JQ = 4;  // query quarters per boundary (blockIdx.y): 4x the loads in flight
+static_assert(kSplitMaxCtas * (1 + COMBINE_JQ) <= 1024, "partials array: max(num_tiles, 1024) entries");
+__global__ void __launch_bounds__(BM) split_combine_kernel(const double *__restrict__ split, int64_t T, int nq,
+                                                           int64_t ntiles, int ngrp, int G, Partial *partials) {
+    constexpr int JN = BN / COMBINE_JQ;
+    const int k = blockIdx.x, r = threadIdx.x, j0 = blockIdx.y * JN;
+    const int64_t U = (ntiles % G) * ngrp;  // tail units
+    const int64_t ub = U * (k + 1) / G;      // first tail unit of CTA k+1
+    const int64_t ub_prev = U * k / G;       // first tail unit of CTA k
+    const int64_t tile = ub / ngrp, t0 = tile * ngrp;
+    double attn = 0.0;
+    if (ub % ngrp != 0 && ub_prev <= t0) {
+        const int64_t row = ((ntiles / G) * G + tile) * BM + r;
+        double d[JN];
+#pragma unroll
+        for (int j = 0; j < JN; j++) d[j] = 0.0;
+        for (int c = k; c < G && U * c / G < t0 + ngrp; c++) {
+            if (U * (c + 1) / G == U * c / G) continue;  // empty tail share: no piece
+            const int slot = (U * c / G > t0) ? 0 : 1;
+            const double *sp = split + ((int64_t)c * 2 + slot) * (BN * BM) + (int64_t)j0 * BM;
+#pragma unroll
+            for (int j = 0; j < JN; j++)
+                if (j0 + j < nq) d[j] += sp[j * BM + r];
+        }
+        if (row < T)
+#pragma unroll
+            for (int j = 0; j < JN; j++)
+                if (j0 + j < nq) attn += fabs(d[j]);
+    }
+    __shared__ double red[BM];
+    red[r] = attn;
+    __syncthreads();
+    for (int o = BM / 2; o > 0; o >>= 1) {
+        if (r < o) red[r] += red[r + o];
+        __syncthreads();
+    }
+    if (r == 0) partials[G + k * COMBINE_JQ + blockIdx.y] = Partial{0.0, red[0], 0.0, 0.0};
+}
+
 // byte address of 16-byte chunk c of row r in a [rows][128 B] tile with the TMA 128B swizzle
 __device__ __forceinline__ uint32_t swz(uint32_t base, int r, int c) { return base + r * 128 + ((c ^ (r & 7)) << 4); }
 
@@ -167,7 +276,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     Smem &s = *reinterpret_cast<Smem *>(smem_raw);
     const int64_t T = p.T;
-    const int nq = p.nq, ntiles = p.ntiles, nkb = p.nkb, has_khat = p.has_khat;
+    const int nq = p.nq, nkb = p.nkb, has_khat = p.has_khat;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     constexpr int KST = Ring<MODE>::kst;
 
@@ -203,6 +312,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = s.tmem_base;
+    const int ngrp = p.ngrp;
+    const Units us = make_units(p);
 
     if (warp < CONV_W0) {
         setmaxnreg_dec<56>();  // warpgroup 0: producer + MMA issuer need few registers
@@ -212,8 +323,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint64_t pol_keep = policy_evict_last();  // column records: re-read by every tile
             const uint32_t kbytes = (has_khat ? 2 * KTILE : KTILE) + (MODE == 2 ? (uint32_t)sizeof(ColRec) : 0u);
             uint32_t g = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int kb = 0; kb < nkb; kb++, g++) {
+            for (UnitWalk w(us); w.ok(); w.next()) {
+                const int tile = w.tile, kb0 = w.grp * CODE_KB, kb1 = min(kb0 + CODE_KB, nkb);
+                #pragma unroll 1
+                for (int kb = kb0; kb < kb1; kb++, g++) {
                     const int sk = g % KST;
                     mbar_wait_sleep(&s.empty_k[sk], ((g / KST) & 1) ^ 1);
                     mbar_arrive_tx(&s.full_k[sk], kbytes);
@@ -228,8 +341,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // Separate from the K producer so a late MMA never holds back the HBM stream.
             const uint64_t pol_keep = policy_evict_last();
             uint32_t g = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int kb = 0; kb < nkb; kb++, g++) {
+            for (UnitWalk w(us); w.ok(); w.next()) {
+                const int kb0 = w.grp * CODE_KB, kb1 = min(kb0 + CODE_KB, nkb);
+                #pragma unroll 1
+                for (int kb = kb0; kb < kb1; kb++, g++) {
                     const int sq = g % QST;
                     mbar_wait_sleep(&s.empty_q[sq], ((g / QST) & 1) ^ 1);
                     mbar_arrive_tx(&s.full_q[sq], 2 * QTILE);
@@ -246,12 +361,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint64_t pol_out = (p.hints & 2) ? policy_evict_first() : policy_evict_normal();
             uint32_t g = 0, grp = 0;
             bool prev_group_end = false;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int kb = 0; kb < nkb; kb++, g++) {
+            for (UnitWalk w(us); w.ok(); w.next()) {
+                const int tile = w.tile, kb0 = w.grp * CODE_KB, kb1 = min(kb0 + CODE_KB, nkb);
+                #pragma unroll 1
+                for (int kb = kb0; kb < kb1; kb++, g++) {
                     const int sk = g % KST;
                     mbar_wait_sleep(&s.staged[sk], (g / KST) & 1);
                     tma_store_2d(&tmKh, s.buf + sk * Ring<MODE>::stage, kb * BK, tile * BM, pol_out);
-                    const bool group_end = (kb % CODE_KB) == CODE_KB - 1 || kb == nkb - 1;
+                    const bool group_end = kb == kb1 - 1;
                     if (group_end)
                         tma_store_2d(&tmKq, s.buf + 128 * 1024 + (grp & 1) * KTILE, (kb / CODE_KB) * (BK * CODE_KB),
                                      tile * BM, pol_out);
@@ -269,12 +386,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         } else if (warp == 1 && lane == 0) {
             // ------------------------------------------------------------ MMA issuer
             uint32_t g = 0, gc = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int kb = 0; kb < nkb; kb++, g++) {
+            for (UnitWalk w(us); w.ok(); w.next()) {
+                const int kb0 = w.grp * CODE_KB, kb1 = min(kb0 + CODE_KB, nkb);
+                #pragma unroll 1
+                for (int kb = kb0; kb < kb1; kb++, g++) {
                     const int ab = gc & 1;
                     const uint32_t d = tbase + ab * BN;
-                    const bool chunk_first = (kb % CHUNK_KB) == 0;
-                    const bool chunk_last = (kb % CHUNK_KB) == CHUNK_KB - 1 || kb == nkb - 1;
+                    const bool chunk_first = kb == kb0;
+                    const bool chunk_last = kb == kb1 - 1;
                     if (chunk_first) {
                         KVQ_WAIT_HOT(&s.empty_acc[ab], ((gc >> 1) & 1) ^ 1);
                         tc_fence_after();
@@ -313,8 +432,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         double ss = 0.0;
         float mx = 0.0f;
         uint32_t g = 0, cgrp = 0;  // K-block and code-group counters (same order as the store warp)
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            for (int kb = 0; kb < nkb; kb++, g++) {
+        for (UnitWalk w(us); w.ok(); w.next()) {
+            const int kb0 = w.grp * CODE_KB, kb1 = min(kb0 + CODE_KB, nkb);
+            #pragma unroll 1
+            for (int kb = kb0; kb < kb1; kb++, g++) {
                 const int sk = g % KST;
                 KVQ_WAIT_HOT(&s.full_k[sk], (g / KST) & 1);
                 const uint32_t kbase = smem_u32(s.buf + sk * Ring<MODE>::stage);
@@ -378,7 +499,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     // K_hat overwrites x in the input stage (same swizzled positions, read by this
                     // thread only); the codes go to the group's code buffer.  The store warp writes
                     // both out with TMA and then frees the stage (and the code buffer).
-                    if ((kb % CODE_KB) == 0) KVQ_WAIT_HOT(&s.cstored[cgrp & 1], ((cgrp >> 1) & 1) ^ 1);
+                    if (kb == kb0) KVQ_WAIT_HOT(&s.cstored[cgrp & 1], ((cgrp >> 1) & 1) ^ 1);
                     const uint32_t cds = smem_u32(s.buf + 128 * 1024 + (cgrp & 1) * KTILE);
 #pragma unroll
                     for (int c = 0; c < 4; c++)
@@ -392,7 +513,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     sts128u(swz(cds, r, (kb % CODE_KB) * 2 + h), w);
                     fence_proxy_async();  // generic smem writes -> visible to the TMA (async proxy)
                     mbar_arrive(&s.staged[sk]);
-                    if ((kb % CODE_KB) == CODE_KB - 1 || kb == nkb - 1) cgrp++;
+                    if (kb == kb1 - 1) cgrp++;
 #pragma unroll
                     for (int i = 0; i < 16; i++) e[i] = __fsub_rn(x[i], xh[i]);  // exact (fact 4)
                 }
@@ -443,37 +564,48 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         double attn = 0.0;
         uint32_t gc = 0;
-        const int nchunks = (nkb + CHUNK_KB - 1) / CHUNK_KB;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            double acc[BN];
+        double acc[BN];
+        int piece_grp0 = 0;
+        for (UnitWalk w(us); w.ok(); w.next(), gc++) {
+            const int tile = w.tile, grp = w.grp;
+            if (grp == 0 || w.i == w.nfull) {  // first unit of this CTA's piece of the tile
+                piece_grp0 = grp;
 #pragma unroll
-            for (int j = 0; j < BN; j++) acc[j] = 0.0;
-            for (int c = 0; c < nchunks; c++, gc++) {
-                const int ab = gc & 1;
-                mbar_wait_sleep(&s.full_acc[ab], (gc >> 1) & 1);
-                tc_fence_after();
-                uint32_t v[32];
-#pragma unroll
-                for (int hh = 0; hh < BN / 32; hh++) {
-                    tmem_ld32(tbase + lane_off + ab * BN + 32 * hh, v);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int j = 0; j < 32; j++) acc[32 * hh + j] += (double)__uint_as_float(v[j]);
-                }
-                tc_fence_before();
-                mbar_arrive(&s.empty_acc[ab]);
+                for (int j = 0; j < BN; j++) acc[j] = 0.0;
             }
-            const int64_t row = (int64_t)tile * BM + r;
-            if (row < T) {
+            const int ab = gc & 1;
+            mbar_wait_sleep(&s.full_acc[ab], (gc >> 1) & 1);
+            tc_fence_after();
+            uint32_t v[32];
 #pragma unroll
-                for (int j = 0; j < BN; j++) {
-                    if (j < nq) {
-                        if (MODE != 1)
-                            attn += fabs(acc[j]);
-                        else
-                            p.S[(int64_t)j * T + row] = (float)acc[j];
+            for (int hh = 0; hh < BN / 32; hh++) {
+                tmem_ld32(tbase + lane_off + ab * BN + 32 * hh, v);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; j++) acc[32 * hh + j] += (double)__uint_as_float(v[j]);
+            }
+            tc_fence_before();
+            mbar_arrive(&s.empty_acc[ab]);
+            if (w.i != w.n - 1 && grp != ngrp - 1) continue;  // piece not finished
+            if (piece_grp0 == 0 && grp == ngrp - 1) {
+                // the whole tile row-block is this CTA's: Delta is complete
+                const int64_t row = (int64_t)tile * BM + r;
+                if (row < T) {
+#pragma unroll
+                    for (int j = 0; j < BN; j++) {
+                        if (j < nq) {
+                            if (MODE != 1)
+                                attn += fabs(acc[j]);
+                            else
+                                p.S[(int64_t)j * T + row] = (float)acc[j];
+                        }
                     }
                 }
+            } else if (MODE != 1) {
+                // a piece of a split tile: slot 0 if it starts inside the tile, else slot 1
+                double *slot = p.split + ((int64_t)blockIdx.x * 2 + (piece_grp0 != 0 ? 0 : 1)) * (BN * BM);
+#pragma unroll
+                for (int j = 0; j < BN; j++) slot[j * BM + r] = acc[j];
             }
         }
         if (MODE != 1) {
@@ -548,6 +680,11 @@ bool tc_roundtrip_eligible(const float *K, const int8_t *Kq, const float *K_hat,
 
 size_t tc_colq_bytes(int64_t D) { return (size_t)((D + tc::BK - 1) / tc::BK) * sizeof(tc::ColRec); }
 
+size_t tc_split_bytes(int64_t T, int64_t D) {
+    const int64_t nunits = (T + tc::BM - 1) / tc::BM * (((D + tc::BK - 1) / tc::BK + tc::CODE_KB - 1) / tc::CODE_KB);
+    return (size_t)std::min<int64_t>(nunits, kSplitMaxCtas) * 2 * tc::BN * tc::BM * sizeof(double);
+}
+
 template <int MODE>
 static void launch_mode(const CUtensorMap &mK, const CUtensorMap &mKh, const CUtensorMap &mKq, const tc::TcParams &p,
                         int grid, size_t smem, cudaStream_t s) {
@@ -561,7 +698,7 @@ static void launch_mode(const CUtensorMap &mK, const CUtensorMap &mKh, const CUt
 // Launch: qsplit (into ws_q) [+ colq] + the persistent tensor-core kernel.
 kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
                           int64_t nq, void *ws_q, void *partials, int *grid_out, float *S, cudaStream_t s,
-                          const float *scales, void *ws_colq, int8_t *Kq_out, float *Kh_out) {
+                          const float *scales, void *ws_colq, int8_t *Kq_out, float *Kh_out, void *ws_split) {
     using namespace tc;
     const int64_t nkb = (D + BK - 1) / BK;
     const int ntiles = (int)((T + BM - 1) / BM);
@@ -604,16 +741,34 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
         p.colq = cq;
         p.Kh = Kh_out;
     }
-    const int grid = std::min(ntiles, device_info().num_sms);
+    p.ngrp = (int)((nkb + CODE_KB - 1) / CODE_KB);
+    const int64_t nunits = (int64_t)ntiles * p.ngrp;
+    // modes 0/2: whole-tile waves + balanced tail (tiles may be split, see make_units); mode 1: whole tiles
+    // Balanced tail only where whole tiles leave the last wave less than 60% full after at least one
+    // full wave (the C4 shard at 2 ranks: 512 tiles on 148 SMs = 3 waves + 46%; measured 0.98 vs
+    // 1.03 ms).  One wave (the 128 tiles of a C4 shard at 8 ranks), 1.73 waves (4 ranks: balanced
+    // measured 2% slower) and 6.9 waves (C4 on one GPU) stay whole.
+    const int nsm = std::min(device_info().num_sms, kSplitMaxCtas);
+    const int64_t last = ntiles % nsm;  // tiles in the partial last wave
+    const char *force = std::getenv("KVQ_TC_BALANCE");  // experiments: 0 = whole tiles, 1 = balanced tail
+    const bool want = force ? force[0] == '1' : (ntiles > nsm && last > 0 && last * 10 < nsm * 6);
+    const bool balanced = mode != 1 && ws_split != nullptr && want;
+    const int grid = !balanced ? std::min(ntiles, device_info().num_sms) : (int)std::min<int64_t>(nunits, nsm);
+    p.split = balanced ? reinterpret_cast<double *>(ws_split) : nullptr;
     const size_t smem = sizeof(Smem);
-    if (grid_out) *grid_out = grid;
+    if (grid_out) *grid_out = balanced ? grid + COMBINE_JQ * (grid - 1) : grid;  // + per CTA boundary and quarter
     if (mode == 0)
         launch_mode<0>(mK, mKh, mKq, p, grid, smem, s);
     else if (mode == 1)
         launch_mode<1>(mK, mKh, mKq, p, grid, smem, s);
     else
         launch_mode<2>(mK, mKh, mKq, p, grid, smem, s);
-    return check_launch(mode == 0 ? "attn_tc(metrics)" : mode == 1 ? "attn_tc(scores)" : "attn_tc(roundtrip)");
+    if (kvq_status st = check_launch(mode == 0 ? "attn_tc(metrics)" : mode == 1 ? "attn_tc(scores)" : "attn_tc(roundtrip)");
+        st != KVQ_OK || !balanced || grid == 1)
+        return st;
+    split_combine_kernel<<<dim3(grid - 1, COMBINE_JQ), BM, 0, s>>>(p.split, T, (int)nq, ntiles, p.ngrp, grid,
+                                                 reinterpret_cast<Partial *>(partials));
+    return check_launch("attn_tc(split_combine)");
 }
 
 }  // namespace kvq

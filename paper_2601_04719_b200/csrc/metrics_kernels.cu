@@ -237,6 +237,7 @@ struct WsLayout {
     Partial *partials;
     void *qsplit;
     void *colq;
+    void *split;  // tensor-core kernels: fp64 Delta of tiles split between CTAs
     double *sums;
     uint64_t *maxes;
 };
@@ -252,6 +253,8 @@ static WsLayout ws_layout(void *ws, int64_t T, int64_t D) {
     off += al256(tc_qsplit_bytes(D));
     L.colq = reinterpret_cast<void *>(off);
     off += al256(tc_colq_bytes(D));
+    L.split = reinterpret_cast<void *>(off);
+    off += al256(tc_split_bytes(T, D));
     L.sums = reinterpret_cast<double *>(off);
     L.maxes = reinterpret_cast<uint64_t *>(L.sums + 4);
     return L;
@@ -261,7 +264,7 @@ size_t metrics_workspace_size(int64_t T, int64_t D, int64_t nq) {
     (void)nq;
     const size_t np = (size_t)std::max<int64_t>(num_tiles(T), 1024);
     return 256 + al256(np * sizeof(Partial)) + al256(tc_qsplit_bytes(D)) + al256(tc_colq_bytes(D)) +
-           4 * sizeof(double) + 2 * sizeof(uint64_t);
+           al256(tc_split_bytes(T, D)) + 4 * sizeof(double) + 2 * sizeof(uint64_t);
 }
 
 static kvq_status reduce_partials(const WsLayout &L, int64_t nparts, const float *scales, int64_t T, int64_t D,
@@ -282,7 +285,8 @@ kvq_status launch_metrics_partials(const float *K, const float *K_hat, int64_t T
     int64_t nparts;
     if (!force_simt() && tc_eligible(K, K_hat, T, D, nq)) {
         int grid = 0;
-        if (kvq_status st = launch_attn_tc(0, K, K_hat, T, D, Q, nq, L.qsplit, L.partials, &grid, nullptr, s);
+        if (kvq_status st = launch_attn_tc(0, K, K_hat, T, D, Q, nq, L.qsplit, L.partials, &grid, nullptr, s, nullptr, nullptr,
+                                                nullptr, nullptr, L.split);
             st != KVQ_OK)
             return st;
         nparts = grid;
@@ -303,7 +307,7 @@ kvq_status launch_roundtrip_partials(const float *K, const float *scales, int64_
         const WsLayout L = ws_layout(ws, T, D);
         int grid = 0;
         if (kvq_status st = launch_attn_tc(2, K, nullptr, T, D, Q, nq, L.qsplit, L.partials, &grid, nullptr, s,
-                                           scales, L.colq, Kq, K_hat);
+                                           scales, L.colq, Kq, K_hat, L.split);
             st != KVQ_OK)
             return st;
         return reduce_partials(L, grid, scales, T, D, nq, totals, s);

@@ -463,6 +463,57 @@ def test_roundtrip_single_pass_vs_oracle(kvq, orc, T, D, nq, dist):
         assert _rel(m["attn_mean_abs"], orc.attention_error(Q, K, kho)) <= REL
 
 
+# Balanced tail (attn_tc.cu make_units): tiles split between CTAs, their Delta pieces added by
+# split_combine_kernel.  Forced on (KVQ_TC_BALANCE=1) so that small shapes split: every tile in 16 / ~10
+# pieces, ragged T, one whole-tile wave + a 1-tile tail in 2 units (most tail shares empty), one-unit
+# tiles (no split possible), nq < 64 (query quarters partly empty), and the default rule on C4-shard
+# shapes (3.46 waves: balanced; 128 tiles: whole).
+SPLIT_CASES = [(640, 2048, 64), (2000, 8192, 64), (19072, 256, 64), (19200, 32, 64), (19100, 1024, 33),
+               (300, 4096, 17)]
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("T,D,nq", SPLIT_CASES)
+@pytest.mark.parametrize("fn", ["metrics", "roundtrip"])
+def test_balanced_split_tiles_vs_oracle(kvq, orc, monkeypatch, T, D, nq, fn):
+    monkeypatch.setenv("KVQ_TC_BALANCE", "1")
+    K = orc.fill(T, D, 7, 1)
+    so, qo, kho = orc.roundtrip(K)
+    Q = orc.fill(nq, D, 43)
+    Kd = dev(K)
+    if fn == "metrics":
+        m = kvq.kvq_error_metrics(Kd, dev(kho), dev(Q), dev(so))
+    else:
+        s = kvq.kvq_compute_scales(Kd)
+        Kq, Kh, out = kvq.kvq_roundtrip(Kd, s, dev(Q))
+        m = kvq.metrics_from_device(out)
+        same_bits(host(Kq), qo)
+        same_bits(host(Kh), kho)
+    ss, mx = orc.recon_errors(K, kho)
+    assert m["max_abs"] == mx and _rel(m["sum_sq"], ss) <= REL
+    assert m["n_scores"] == nq * T
+    assert _rel(m["attn_mean_abs"], orc.attention_error(Q, K, kho)) <= REL
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("balance", ["0", "1"])
+def test_balanced_and_whole_tiles_agree(kvq, orc, monkeypatch, balance):
+    """Same metrics (to fp64 rounding) whether the 3.46-wave shape runs balanced or as whole tiles."""
+    T, D, nq = 65536 // 8, 8192, 64  # 64 tiles: forced balance splits every tile of the one wave
+    K = kvq.kvq_synth_fill(T, D, seed=42)
+    Q = kvq.kvq_synth_fill(nq, D, seed=43)
+    s = kvq.kvq_compute_scales(K)
+    monkeypatch.setenv("KVQ_TC_BALANCE", balance)
+    _, _, out = kvq.kvq_roundtrip(K, s, Q)
+    m = kvq.metrics_from_device(out)
+    monkeypatch.setenv("KVQ_TC_BALANCE", "0")
+    _, _, out0 = kvq.kvq_roundtrip(K, s, Q)
+    m0 = kvq.metrics_from_device(out0)
+    assert m["max_abs"] == m0["max_abs"]
+    assert _rel(m["attn_mean_abs"], m0["attn_mean_abs"]) <= 1e-12
+    assert _rel(m["sum_sq"], m0["sum_sq"]) <= 1e-12
+
+
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("name", ["ties", "subnormal", "underflow", "zeros", "mixed"])
 def test_roundtrip_structured_inputs(kvq, orc, name):
