@@ -209,6 +209,28 @@ def run_reference(args, cfg, rank, world):
 
 
 # ----------------------------------------------------------------------------- the GPU arm
+def launches_per_step(args, comm, comm_kind, rows, D):
+    """libkvq kernels one step launches (NCCL's own kernels and memsets not counted), per csrc/:
+    scales = colmax + finalize (one fused column-max/exchange/finalize kernel with a peer communicator);
+    roundtrip = prep (Q split + column records) + attn_tc<2> [+ split_combine when the tail is balanced]
+    + reduce_partials (which also writes the result when there is no communicator); metrics alone =
+    qsplit + attn_tc<0> [+ split_combine] + reduce_partials; a communicator adds metrics_finalize, and the
+    peer one also its metric-exchange kernel."""
+    import torch
+    nsm = min(torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count, 160)
+    ntiles = (rows + 127) // 128
+    combine = 1 if (ntiles > nsm and 0 < ntiles % nsm and (ntiles % nsm) * 10 < nsm * 6) else 0
+    peer = comm is not None and comm_kind is not None and comm_kind.startswith("peer")
+    scales = 1 if peer else 2
+    tail = 0 if comm is None else (2 if peer else 1)
+    if args.format == "int8" and args.pipeline == "fused":
+        return scales + 3 + combine + tail
+    metrics = 3 + combine + tail
+    if args.format == "int8":
+        return scales + 1 + 1 + metrics  # + quantize + dequantize
+    return scales + 1 + metrics          # + the format's fused quantize+dequantize
+
+
 def run_kvq(args, cfg, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -471,9 +493,8 @@ def run_kvq(args, cfg, rank, world, local_rank):
         "hbm": {"GBps": algo_bytes / (ms * 1e-3) / 1e9 / world, "algo_bytes_per_elem": algo_per_elem,
                 "frac_of_peak_per_gpu": algo_bytes / (ms * 1e-3) / 1e9 / world / pk["hbm_gbs"]},
         "passes": pass_report, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        # (a peer communicator replaces the finalize kernel by the fused exchange and adds one metric-exchange
-        # kernel: the count is the same; NCCL's kernels are not counted)
-        "gpu_launches": (7 if args.format != "int8" else 7 if args.pipeline == "fused" else 8) * args.steps, "clocks": clk.summary(wall0, wall1),
+        "gpu_launches": launches_per_step(args, comm, comm_kind, rows, D) * args.steps,
+        "clocks": clk.summary(wall0, wall1),
         "fidelity": {k: metrics[k] for k in ("l2", "max_abs", "attn_mean_abs", "theoretical_max")},
     }
     print(json.dumps(line), flush=True)

@@ -338,11 +338,11 @@ extern "C" kvq_status kvq_error_metrics_async(const float *K, const float *K_hat
     KVQ_TRY(device_ok());
     cudaStream_t s = (cudaStream_t)stream;
     MetricTotals tot;
+    if (!comm) tot.fused_out = out_dev;  // nothing to exchange: the reduction writes the result
     KVQ_TRY(launch_metrics_partials(K, K_hat, T, D, nq ? Q : nullptr, nq, scales, workspace, workspace_bytes, &tot,
                                     s));
-    if (comm) {
-        KVQ_TRY(comm_allreduce_metrics(comm, tot.sums, 4, tot.maxes, 2, s));
-    }
+    if (!comm) return KVQ_OK;
+    KVQ_TRY(comm_allreduce_metrics(comm, tot.sums, 4, tot.maxes, 2, s));
     return launch_metrics_finalize(tot, out_dev, s);
 }
 
@@ -381,11 +381,11 @@ extern "C" kvq_status kvq_roundtrip(const float *K, const float *scales, int64_t
     KVQ_TRY(device_ok());
     cudaStream_t s = (cudaStream_t)stream;
     MetricTotals tot;
+    if (!comm) tot.fused_out = out_dev;  // nothing to exchange: the reduction writes the result
     KVQ_TRY(launch_roundtrip_partials(K, scales, T, D, Kq, K_hat, nq ? Q : nullptr, nq, workspace, workspace_bytes,
                                       &tot, s));
-    if (comm) {
-        KVQ_TRY(comm_allreduce_metrics(comm, tot.sums, 4, tot.maxes, 2, s));
-    }
+    if (!comm) return KVQ_OK;
+    KVQ_TRY(comm_allreduce_metrics(comm, tot.sums, 4, tot.maxes, 2, s));
     return launch_metrics_finalize(tot, out_dev, s);
 }
 

@@ -111,7 +111,7 @@ struct TcParams {
     int nq, ntiles, nkb, has_khat;
     Partial *partials;   // MODE 0, 2: one per CTA
     float *S;            // MODE 1: [nq][T]
-    const ColRec *colq;  // MODE 2: per K-block quantizer records (colq_kernel)
+    const ColRec *colq;  // MODE 2: per K-block quantizer records (colq_body, in prep_kernel)
     int hints;           // L2 policies: bit0 K loads evict-first, bit1 output stores evict-first (default both;
                          // evict-first loads with normal stores cost ~0.6 GB of extra DRAM reads at C4)
     float *Kh;           // MODE 2: K_hat output [T][D]
@@ -182,10 +182,10 @@ static_assert(CHUNK_KB == CODE_KB, "one accumulator chunk per work unit");
 // K-major SWIZZLE_NONE layout: core matrix (kg = k/4, rg = n/8) at byte
 // (kg*8 + rg)*128, row n%8 at +16*(n%8), element k%4 at +4*(k%4).  Rows >= nq
 // and columns >= D are zero.
-__global__ void qsplit_kernel(const float *__restrict__ Q, int64_t nq, int64_t D, int64_t nkb,
-                              uint32_t *__restrict__ out) {
+__device__ __forceinline__ void qsplit_body(const float *__restrict__ Q, int64_t nq, int64_t D, int64_t nkb,
+                                            uint32_t *__restrict__ out, int64_t blk, int64_t nblk) {
     const int64_t total = nkb * BN * BK;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = blk * blockDim.x + threadIdx.x; i < total; i += nblk * blockDim.x) {
         const int64_t kb = i / (BN * BK);
         const int rem = (int)(i % (BN * BK));
         const int n = rem / BK, k = rem % BK;
@@ -200,21 +200,40 @@ __global__ void qsplit_kernel(const float *__restrict__ Q, int64_t nq, int64_t D
     }
 }
 
+__global__ void qsplit_kernel(const float *__restrict__ Q, int64_t nq, int64_t D, int64_t nkb,
+                              uint32_t *__restrict__ out) {
+    qsplit_body(Q, nq, D, nkb, out, blockIdx.x, gridDim.x);
+}
+
 // Per-K-block quantizer records for the fused kernel: {s, RN(1/s)} per column,
 // with y = 0 for s == 0 (code 0) and for subnormal/huge s, which need the exact
 // path (flagged per block).
-__global__ void colq_kernel(const float *__restrict__ scales, int64_t D, int64_t nkb, ColRec *__restrict__ out) {
-    for (int64_t kb = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; kb < nkb; kb += (int64_t)gridDim.x * blockDim.y) {
-        const int64_t d = kb * BK + threadIdx.x;
+// (256-thread blocks: lane = column of the K-block, warp = K-block slot)
+__device__ __forceinline__ void colq_body(const float *__restrict__ scales, int64_t D, int64_t nkb,
+                                          ColRec *__restrict__ out, int64_t blk, int64_t nblk) {
+    const int lx = threadIdx.x % 32, ly = threadIdx.x / 32;
+    for (int64_t kb = blk * 8 + ly; kb < nkb; kb += nblk * 8) {
+        const int64_t d = kb * BK + lx;
         const float sd = d < D ? scales[d] : 0.0f;
         const ColQ c = make_colq(sd);
-        out[kb].c[threadIdx.x] = make_float2(sd, c.y);
+        out[kb].c[lx] = make_float2(sd, c.y);
         const unsigned any = __ballot_sync(0xffffffffu, c.exact);
-        if (threadIdx.x == 0) {
+        if (lx == 0) {
             out[kb].any_exact = any ? 1u : 0u;
             out[kb].pad[0] = out[kb].pad[1] = out[kb].pad[2] = 0u;
         }
     }
+}
+
+// The fused mode's two small preparation passes in one launch: blocks [0, nbq) split Q, the rest build
+// the column records.
+__global__ void __launch_bounds__(256) prep_kernel(const float *__restrict__ Q, int64_t nq, int64_t D, int64_t nkb,
+                                                   uint32_t *__restrict__ qs, const float *__restrict__ scales,
+                                                   ColRec *__restrict__ cq, int nbq) {
+    if ((int)blockIdx.x < nbq)
+        qsplit_body(Q, nq, D, nkb, qs, blockIdx.x, nbq);
+    else
+        colq_body(scales, D, nkb, cq, blockIdx.x - nbq, gridDim.x - nbq);
 }
 
 // Split tiles (see make_units): block k < G-1 looks at the boundary between the tail shares of CTAs k
@@ -714,10 +733,9 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
         if (!make_map_f32(&mKh, K_hat, T, D)) return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(K_hat) failed");
     }
     uint32_t *qs = reinterpret_cast<uint32_t *>(ws_q);
-    {
-        const int64_t total = nkb * BN * BK;
-        const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 4096);
-        qsplit_kernel<<<blocks, 256, 0, s>>>(Q, nq, D, nkb, qs);
+    const unsigned qblocks = (unsigned)std::min<int64_t>((nkb * BN * BK + 255) / 256, 4096);
+    if (mode != 2) {
+        qsplit_kernel<<<qblocks, 256, 0, s>>>(Q, nq, D, nkb, qs);
         if (kvq_status st = check_launch("qsplit"); st != KVQ_OK) return st;
     }
     TcParams p{};
@@ -736,8 +754,9 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
     }
     if (mode == 2) {
         ColRec *cq = reinterpret_cast<ColRec *>(ws_colq);
-        colq_kernel<<<(unsigned)std::min<int64_t>((nkb + 7) / 8, 1024), dim3(32, 8), 0, s>>>(scales, D, nkb, cq);
-        if (kvq_status st = check_launch("colq"); st != KVQ_OK) return st;
+        const unsigned cblocks = (unsigned)std::min<int64_t>((nkb + 7) / 8, 1024);
+        prep_kernel<<<qblocks + cblocks, 256, 0, s>>>(Q, nq, D, nkb, qs, scales, cq, (int)qblocks);
+        if (kvq_status st = check_launch("qsplit+colq"); st != KVQ_OK) return st;
         p.colq = cq;
         p.Kh = Kh_out;
     }

@@ -70,6 +70,8 @@ kvq_status launch_single_pass(const float *K, int64_t T, int64_t D, float *scale
 struct MetricTotals {
     double *sums;      // [4] device
     uint64_t *maxes;   // [2] device
+    kvq_metrics *fused_out = nullptr;  // set by the caller when no exchange follows: the reduction kernel
+                                       // then also writes the final struct (no metrics_finalize launch)
 };
 struct Partial {  // per-CTA partial sums of a5/a6
     double sum_sq, attn_abs, max_abs, pad;

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256) attn_tile_kernel(const float *__restrict_
 __global__ void __launch_bounds__(1024) reduce_partials_kernel(const Partial *__restrict__ partials, int64_t np,
                                                                const float *__restrict__ scales, int64_t D,
                                                                double n_elems, double n_scores, double *sums,
-                                                               uint64_t *maxes) {
+                                                               uint64_t *maxes, kvq_metrics *out) {
     __shared__ double sh[3][1024];
     const int tid = threadIdx.x;
     double ss = 0.0, at = 0.0, mx = 0.0, th = 0.0;
@@ -206,6 +206,18 @@ __global__ void __launch_bounds__(1024) reduce_partials_kernel(const Partial *__
         sums[3] = n_scores;
         maxes[0] = (uint64_t)__double_as_longlong(maxabs);
         maxes[1] = (uint64_t)__double_as_longlong(sh[2][0]);
+        if (out) {  // single process: the final struct too (same arithmetic as metrics_finalize_kernel)
+            kvq_metrics m;
+            m.sum_sq = sh[0][0];
+            m.attn_abs_sum = sh[1][0];
+            m.n_elems = (int64_t)n_elems;
+            m.n_scores = (int64_t)n_scores;
+            m.l2 = sqrt(sh[0][0]);
+            m.max_abs = maxabs;
+            m.theoretical_max = sh[2][0];
+            m.attn_mean_abs = n_scores > 0.0 ? sh[1][0] / n_scores : 0.0;
+            *out = m;
+        }
     }
 }
 
@@ -272,7 +284,7 @@ static kvq_status reduce_partials(const WsLayout &L, int64_t nparts, const float
     totals->sums = L.sums;
     totals->maxes = L.maxes;
     reduce_partials_kernel<<<1, 1024, 0, s>>>(L.partials, nparts, scales, D, (double)T * (double)D,
-                                              (double)nq * (double)T, L.sums, L.maxes);
+                                              (double)nq * (double)T, L.sums, L.maxes, totals->fused_out);
     return check_launch("metrics_reduce");
 }
 
