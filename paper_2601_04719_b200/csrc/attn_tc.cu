@@ -184,22 +184,27 @@ static_assert(CHUNK_KB == CODE_KB, "one accumulator chunk per work unit");
 // and columns >= D are zero.
 __device__ __forceinline__ void qsplit_body(const float *__restrict__ Q, int64_t nq, int64_t D, int64_t nkb,
                                             uint32_t *__restrict__ out, int64_t blk, int64_t nblk) {
-    const int64_t total = nkb * BN * BK;
+    // one thread per (K-block, query row, group of 4 columns): the 4 columns of a group are adjacent words of
+    // one core-matrix row, so hi and lo each leave as one 16-byte store
+    const int64_t total = nkb * BN * (BK / 4);
     for (int64_t i = blk * blockDim.x + threadIdx.x; i < total; i += nblk * blockDim.x) {
-        const int64_t kb = i / (BN * BK);
-        const int rem = (int)(i % (BN * BK));
-        const int n = rem / BK, k = rem % BK;
-        const int64_t col = kb * BK + k;
-        const float q = (n < nq && col < D) ? Q[n * D + col] : 0.0f;
-        const uint32_t hi = to_tf32(q);
-        const uint32_t lo = to_tf32(q - __uint_as_float(hi));
-        const uint32_t off = ((k / 4) * 8 + n / 8) * 32 + (n % 8) * 4 + (k % 4);  // in 4-byte words
+        const int64_t kb = i / (BN * (BK / 4));
+        const int rem = (int)(i % (BN * (BK / 4)));
+        const int n = rem / (BK / 4), kg = rem % (BK / 4);
+        const int64_t col = kb * BK + kg * 4;
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const float q = (n < nq && col + e < D) ? Q[n * D + col + e] : 0.0f;
+            hi[e] = to_tf32(q);
+            lo[e] = to_tf32(q - __uint_as_float(hi[e]));
+        }
+        const uint32_t off = (kg * 8 + n / 8) * 32 + (n % 8) * 4;  // in 4-byte words (16-byte aligned)
         uint32_t *tile = out + kb * (2 * BN * BK);
-        tile[off] = hi;
-        tile[BN * BK + off] = lo;
+        *reinterpret_cast<uint4 *>(tile + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4 *>(tile + BN * BK + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
 }
-
 __global__ void qsplit_kernel(const float *__restrict__ Q, int64_t nq, int64_t D, int64_t nkb,
                               uint32_t *__restrict__ out) {
     qsplit_body(Q, nq, D, nkb, out, blockIdx.x, gridDim.x);
@@ -733,7 +738,7 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
         if (!make_map_f32(&mKh, K_hat, T, D)) return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(K_hat) failed");
     }
     uint32_t *qs = reinterpret_cast<uint32_t *>(ws_q);
-    const unsigned qblocks = (unsigned)std::min<int64_t>((nkb * BN * BK + 255) / 256, 4096);
+    const unsigned qblocks = (unsigned)std::min<int64_t>((nkb * BN * (BK / 4) + 255) / 256, 4096);
     if (mode != 2) {
         qsplit_kernel<<<qblocks, 256, 0, s>>>(Q, nq, D, nkb, qs);
         if (kvq_status st = check_launch("qsplit"); st != KVQ_OK) return st;

@@ -168,8 +168,10 @@ __global__ void __launch_bounds__(1024) reduce_partials_kernel(const Partial *__
                                                                const float *__restrict__ scales, int64_t D,
                                                                double n_elems, double n_scores, double *sums,
                                                                uint64_t *maxes, kvq_metrics *out) {
-    __shared__ double sh[3][1024];
-    const int tid = threadIdx.x;
+    // fixed-order two-level reduction (xor butterfly within each warp, then warp 0 over the 32 warp
+    // results): deterministic, and 2 barriers instead of a 10-level shared-memory tree per quantity
+    __shared__ double sh[4][32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     double ss = 0.0, at = 0.0, mx = 0.0, th = 0.0;
     for (int64_t i = tid; i < np; i += 1024) {
         ss += partials[i].sum_sq;
@@ -178,44 +180,48 @@ __global__ void __launch_bounds__(1024) reduce_partials_kernel(const Partial *__
     }
     if (scales)
         for (int64_t d = tid; d < D; d += 1024) th = fmax(th, (double)scales[d] / 2.0);
-    sh[0][tid] = ss;
-    sh[1][tid] = at;
-    sh[2][tid] = fmax(mx, 0.0);
-    __syncthreads();
-    for (int s = 512; s > 0; s >>= 1) {
-        if (tid < s) {
-            sh[0][tid] += sh[0][tid + s];
-            sh[1][tid] += sh[1][tid + s];
-            sh[2][tid] = fmax(sh[2][tid], sh[2][tid + s]);
-        }
-        __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) {
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        at += __shfl_xor_sync(0xffffffffu, at, o);
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        th = fmax(th, __shfl_xor_sync(0xffffffffu, th, o));
     }
-    // theoretical max: separate max tree (reuse sh[2] after reading the max)
-    const double maxabs = sh[2][0];
-    __syncthreads();
-    sh[2][tid] = th;
-    __syncthreads();
-    for (int s = 512; s > 0; s >>= 1) {
-        if (tid < s) sh[2][tid] = fmax(sh[2][tid], sh[2][tid + s]);
-        __syncthreads();
+    if (lane == 0) {
+        sh[0][wid] = ss;
+        sh[1][wid] = at;
+        sh[2][wid] = mx;
+        sh[3][wid] = th;
     }
+    __syncthreads();
+    if (wid != 0) return;
+    ss = sh[0][lane];
+    at = sh[1][lane];
+    mx = sh[2][lane];
+    th = sh[3][lane];
+    for (int o = 16; o > 0; o >>= 1) {
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        at += __shfl_xor_sync(0xffffffffu, at, o);
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        th = fmax(th, __shfl_xor_sync(0xffffffffu, th, o));
+    }
+    const double maxabs = fmax(mx, 0.0);
     if (tid == 0) {
-        sums[0] = sh[0][0];
-        sums[1] = sh[1][0];
+        sums[0] = ss;
+        sums[1] = at;
         sums[2] = n_elems;
         sums[3] = n_scores;
         maxes[0] = (uint64_t)__double_as_longlong(maxabs);
-        maxes[1] = (uint64_t)__double_as_longlong(sh[2][0]);
+        maxes[1] = (uint64_t)__double_as_longlong(th);
         if (out) {  // single process: the final struct too (same arithmetic as metrics_finalize_kernel)
             kvq_metrics m;
-            m.sum_sq = sh[0][0];
-            m.attn_abs_sum = sh[1][0];
+            m.sum_sq = ss;
+            m.attn_abs_sum = at;
             m.n_elems = (int64_t)n_elems;
             m.n_scores = (int64_t)n_scores;
-            m.l2 = sqrt(sh[0][0]);
+            m.l2 = sqrt(ss);
             m.max_abs = maxabs;
-            m.theoretical_max = sh[2][0];
-            m.attn_mean_abs = n_scores > 0.0 ? sh[1][0] / n_scores : 0.0;
+            m.theoretical_max = th;
+            m.attn_mean_abs = n_scores > 0.0 ? at / n_scores : 0.0;
             *out = m;
         }
     }
