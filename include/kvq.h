@@ -229,7 +229,10 @@ kvq_status kvq_compute_scales_peer(const float *K, int64_t T, int64_t D, float *
  * all-reduced so every rank receives the global metrics.
  * a6 runs on the tcgen05 tensor cores (3xTF32) when 1 <= nq <= 64, D % 4 == 0
  * and K/K_hat are 16-byte aligned, else on the CUDA cores.  Sums are carried in
- * fp64 and reduced with a fixed tree (deterministic run to run). */
+ * fp64 and reduced with a fixed tree (deterministic run to run).  The workspace
+ * holds per-CTA partials, the split Q tiles, per-K-block column records and, for
+ * tiles the tensor-core pass splits between CTAs, up to 160 x 128 KB of fp64
+ * partial scores (the size function accounts for all of it). */
 size_t kvq_error_metrics_workspace_size(int64_t T, int64_t D, int64_t nq);
 kvq_status kvq_error_metrics_async(const float *K, const float *K_hat, int64_t T, int64_t D,
                                    const float *Q, int64_t nq, const float *scales,

@@ -22,6 +22,14 @@ kvq_status fail(kvq_status st, const std::string &msg) {
     return st;
 }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("KVQ_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 kvq_status check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(KVQ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));

@@ -207,6 +207,8 @@ __device__ __forceinline__ void qsplit_body(const float *__restrict__ Q, int64_t
 }
 __global__ void qsplit_kernel(const float *__restrict__ Q, int64_t nq, int64_t D, int64_t nkb,
                               uint32_t *__restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     qsplit_body(Q, nq, D, nkb, out, blockIdx.x, gridDim.x);
 }
 
@@ -235,6 +237,8 @@ __device__ __forceinline__ void colq_body(const float *__restrict__ scales, int6
 __global__ void __launch_bounds__(256) prep_kernel(const float *__restrict__ Q, int64_t nq, int64_t D, int64_t nkb,
                                                    uint32_t *__restrict__ qs, const float *__restrict__ scales,
                                                    ColRec *__restrict__ cq, int nbq) {
+    pdl_wait();  // Q and the scales of the preceding calls
+    pdl_trigger();
     if ((int)blockIdx.x < nbq)
         qsplit_body(Q, nq, D, nkb, qs, blockIdx.x, nbq);
     else
@@ -256,6 +260,8 @@ __global__ void __launch_bounds__(BM) split_combine_kernel(const double *__restr
     const int64_t ub = U * (k + 1) / G;      // first tail unit of CTA k+1
     const int64_t ub_prev = U * k / G;       // first tail unit of CTA k
     const int64_t tile = ub / ngrp, t0 = tile * ngrp;
+    pdl_wait();  // the pieces written by the tensor-core pass
+    pdl_trigger();
     double attn = 0.0;
     if (ub % ngrp != 0 && ub_prev <= t0) {
         const int64_t row = ((ntiles / G) * G + tile) * BM + r;
@@ -336,6 +342,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = s.tmem_base;
+    // everything above (barrier init, TMEM allocation, tensor-map prefetch) overlaps the preceding grid;
+    // from here on the pass reads Q tiles / column records of the preparation kernel and writes outputs
+    pdl_wait();
+    pdl_trigger();
     const int ngrp = p.ngrp;
     const Units us = make_units(p);
 
@@ -716,7 +726,7 @@ static void launch_mode(const CUtensorMap &mK, const CUtensorMap &mKh, const CUt
     std::call_once(once, [&] {
         cudaFuncSetAttribute(tc::attn_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     });
-    tc::attn_tc_kernel<MODE><<<grid, tc::NTHREADS, smem, s>>>(mK, mKh, mKq, p);
+    (void)launch_pdl(tc::attn_tc_kernel<MODE>, dim3(grid), dim3(tc::NTHREADS), smem, s, mK, mKh, mKq, p);
 }
 
 // Launch: qsplit (into ws_q) [+ colq] + the persistent tensor-core kernel.
@@ -740,7 +750,7 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
     uint32_t *qs = reinterpret_cast<uint32_t *>(ws_q);
     const unsigned qblocks = (unsigned)std::min<int64_t>((nkb * BN * (BK / 4) + 255) / 256, 4096);
     if (mode != 2) {
-        qsplit_kernel<<<qblocks, 256, 0, s>>>(Q, nq, D, nkb, qs);
+        (void)launch_pdl(qsplit_kernel, dim3(qblocks), dim3(256), 0, s, Q, nq, D, nkb, qs);
         if (kvq_status st = check_launch("qsplit"); st != KVQ_OK) return st;
     }
     TcParams p{};
@@ -760,7 +770,8 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
     if (mode == 2) {
         ColRec *cq = reinterpret_cast<ColRec *>(ws_colq);
         const unsigned cblocks = (unsigned)std::min<int64_t>((nkb + 7) / 8, 1024);
-        prep_kernel<<<qblocks + cblocks, 256, 0, s>>>(Q, nq, D, nkb, qs, scales, cq, (int)qblocks);
+        (void)launch_pdl(prep_kernel, dim3(qblocks + cblocks), dim3(256), 0, s, Q, nq, D, nkb, qs, scales, cq,
+                         (int)qblocks);
         if (kvq_status st = check_launch("qsplit+colq"); st != KVQ_OK) return st;
         p.colq = cq;
         p.Kh = Kh_out;
@@ -790,8 +801,8 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
     if (kvq_status st = check_launch(mode == 0 ? "attn_tc(metrics)" : mode == 1 ? "attn_tc(scores)" : "attn_tc(roundtrip)");
         st != KVQ_OK || !balanced || grid == 1)
         return st;
-    split_combine_kernel<<<dim3(grid - 1, COMBINE_JQ), BM, 0, s>>>(p.split, T, (int)nq, ntiles, p.ngrp, grid,
-                                                 reinterpret_cast<Partial *>(partials));
+    (void)launch_pdl(split_combine_kernel, dim3(grid - 1, COMBINE_JQ), dim3(BM), 0, s, (const double *)p.split, T,
+                     (int)nq, (int64_t)ntiles, p.ngrp, grid, reinterpret_cast<Partial *>(partials));
     return check_launch("attn_tc(split_combine)");
 }
 

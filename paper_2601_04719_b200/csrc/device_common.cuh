@@ -126,4 +126,8 @@ __device__ __forceinline__ float code_to_float(uint32_t w, int j) {
     return (float)(int)(int8_t)((w >> (8 * j)) & 0xffu);
 }
 
+// Programmatic dependent launch (kvq_internal.h launch_pdl): no-ops when launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace kvq

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "../../include/kvq.h"
 
@@ -124,5 +125,30 @@ kvq_status comm_allreduce_sum_f64(kvq_comm_t comm, double *buf, size_t count, cu
 kvq_status comm_allreduce_max_u64(kvq_comm_t comm, uint64_t *buf, size_t count, cudaStream_t s);
 kvq_status comm_allreduce_metrics(kvq_comm_t comm, double *sums, size_t nsum, uint64_t *maxes, size_t nmax,
                                   cudaStream_t s);
+
+// Programmatic dependent launch for the step's chained kernels (finalize, prep/qsplit, the tensor-core
+// pass, split_combine, the partials reduction, metrics_finalize): the launch of kernel i+1 and its prologue
+// overlap kernel i's tail; every such kernel executes griddepcontrol.wait (pdl_wait) before its first
+// global-memory access, which returns once all prerequisite grids have completed and their writes are
+// visible, so the stream order of memory effects is unchanged.  Each kernel triggers its dependents only
+// after its own wait, so a grid never launches before its predecessor's predecessor has completed (no two
+// tensor-core grids ever hold TMEM on one SM).  The column-max kernel does not trigger early: finalize
+// blocks resident during its stream cost 5-7 us at the 4/8-rank shard sizes (profiles/r01/s4/pdl_ab.txt).
+// KVQ_PDL=0 launches them plainly (A/B).
+bool pdl_enabled();
+template <typename... Exp, typename... Act>
+cudaError_t launch_pdl(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Act &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
+}
 
 }  // namespace kvq

@@ -168,6 +168,8 @@ __global__ void __launch_bounds__(1024) reduce_partials_kernel(const Partial *__
                                                                const float *__restrict__ scales, int64_t D,
                                                                double n_elems, double n_scores, double *sums,
                                                                uint64_t *maxes, kvq_metrics *out) {
+    pdl_wait();  // partials of the preceding tensor-core pass / split_combine
+    pdl_trigger();
     // fixed-order two-level reduction (xor butterfly within each warp, then warp 0 over the 32 warp
     // results): deterministic, and 2 barriers instead of a 10-level shared-memory tree per quantity
     __shared__ double sh[4][32];
@@ -228,6 +230,7 @@ __global__ void __launch_bounds__(1024) reduce_partials_kernel(const Partial *__
 }
 
 __global__ void metrics_finalize_kernel(const double *sums, const uint64_t *maxes, kvq_metrics *out) {
+    pdl_wait();
     kvq_metrics m;
     m.sum_sq = sums[0];
     m.attn_abs_sum = sums[1];
@@ -289,7 +292,7 @@ static kvq_status reduce_partials(const WsLayout &L, int64_t nparts, const float
                                   int64_t nq, MetricTotals *totals, cudaStream_t s) {
     totals->sums = L.sums;
     totals->maxes = L.maxes;
-    reduce_partials_kernel<<<1, 1024, 0, s>>>(L.partials, nparts, scales, D, (double)T * (double)D,
+    (void)launch_pdl(reduce_partials_kernel, dim3(1), dim3(1024), 0, s, L.partials, nparts, scales, D, (double)T * (double)D,
                                               (double)nq * (double)T, L.sums, L.maxes, totals->fused_out);
     return check_launch("metrics_reduce");
 }
@@ -336,7 +339,8 @@ kvq_status launch_roundtrip_partials(const float *K, const float *scales, int64_
 }
 
 kvq_status launch_metrics_finalize(const MetricTotals &t, kvq_metrics *out_dev, cudaStream_t s) {
-    metrics_finalize_kernel<<<1, 1, 0, s>>>(t.sums, t.maxes, out_dev);
+    (void)launch_pdl(metrics_finalize_kernel, dim3(1), dim3(1), 0, s, (const double *)t.sums,
+                     (const uint64_t *)t.maxes, out_dev);
     return check_launch("metrics_finalize");
 }
 

@@ -105,6 +105,8 @@ __global__ void __launch_bounds__(kThreads) colmax_scalar_kernel(const float *__
 // s_d = fl32(m_d / 127.0f), IEEE division (reading Q3); in place.
 // (divisor 448 for the E4M3 variant, reading Q17)
 __global__ void finalize_kernel(uint32_t *buf, int64_t D, float divisor) {
+    pdl_wait();  // the column maxima of the preceding grid
+    pdl_trigger();
     for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < D; d += (int64_t)gridDim.x * blockDim.x) {
         float m = __uint_as_float(buf[d]);
         reinterpret_cast<float *>(buf)[d] = __fdiv_rn(m, divisor);
@@ -510,7 +512,8 @@ kvq_status launch_colmax(const float *K, int64_t T, int64_t D, uint32_t *mbits, 
 
 kvq_status launch_finalize(uint32_t *buf, int64_t D, cudaStream_t s, float divisor) {
     unsigned blocks = (unsigned)std::min<int64_t>((D + 255) / 256, 1024);
-    finalize_kernel<<<blocks, 256, 0, s>>>(buf, D, divisor);
+    if (cudaError_t e = launch_pdl(finalize_kernel, dim3(blocks), dim3(256), 0, s, buf, D, divisor); e != cudaSuccess)
+        return check_launch("finalize");
     return check_launch("finalize");
 }
 

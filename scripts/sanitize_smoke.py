@@ -55,3 +55,14 @@ for D in (64, 13, 1024):
     torch.cuda.synchronize()
     c.destroy()
     p.destroy()
+# balanced tail forced on (tiles split between CTAs, split_combine_kernel), tensor-core metrics and roundtrip
+os.environ["KVQ_TC_BALANCE"] = "1"
+for (T, D, nq) in [(640, 256, 64), (300, 128, 17), (1000, 1024, 33)]:
+    K = kvq.kvq_synth_fill(T, D, seed=42, dist=1)
+    Q = kvq.kvq_synth_fill(nq, D, seed=43)
+    s = kvq.kvq_compute_scales(K)
+    q3, kh3, out = kvq.kvq_roundtrip(K, s, Q)
+    m = kvq.kvq_error_metrics(K, kh3, Q, s)
+    torch.cuda.synchronize()
+    print(T, D, nq, "balanced ok", m["attn_mean_abs"])
+os.environ.pop("KVQ_TC_BALANCE")
