@@ -626,3 +626,27 @@ def test_roundtrip_host_async_pipelined(kvq, orc):
         m = kvq.metrics_from_host(sl["m"])
         assert m["max_abs"] == orc.max_abs_error(sl["K"], kho)
         assert _rel(m["attn_mean_abs"], orc.attention_error(Q, sl["K"], kho)) <= REL
+
+
+@pytest.mark.timeout(300)
+def test_plain_launches_match_pdl_launches(kvq):
+    """KVQ_PDL=0 (plain launches) gives bit-identical codes, K_hat and metrics to the default programmatic
+    dependent launches (the variable is read once per process, hence the subprocess)."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, hashlib; sys.path.insert(0, %r)\n"
+        "from paper_2601_04719_b200 import kvq\n"
+        "K = kvq.kvq_synth_fill(2000, 4096, seed=42, dist=1); Q = kvq.kvq_synth_fill(64, 4096, seed=43)\n"
+        "s = kvq.kvq_compute_scales(K); Kq, Kh, out = kvq.kvq_roundtrip(K, s, Q)\n"
+        "m = kvq.kvq_error_metrics(K, Kh, Q, s)\n"
+        "h = hashlib.sha256(Kq.cpu().numpy().tobytes() + Kh.cpu().numpy().tobytes()).hexdigest()\n"
+        "print(h, repr(kvq.metrics_from_device(out)['attn_mean_abs']), repr(m['attn_mean_abs']), repr(m['sum_sq']))\n"
+    ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for v in ("0", "1"):
+        env = dict(os.environ, KVQ_PDL=v)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=240)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1], outs
