@@ -219,7 +219,10 @@ def launches_per_step(args, comm, comm_kind, rows, D):
     import torch
     nsm = min(torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count, 160)
     ntiles = (rows + 127) // 128
-    combine = 1 if (ntiles > nsm and 0 < ntiles % nsm and (ntiles % nsm) * 10 < nsm * 6) else 0
+    ngrp = ((D + 31) // 32 + 3) // 4  # 4-K-block work units per tile (attn_tc.cu)
+    r0 = ntiles % nsm
+    cut = ntiles >= nsm and r0 > 0 and any(ngrp % c == 0 and r0 * c <= nsm for c in range(2, ngrp + 1))
+    combine = 1 if cut else 0  # left-over tiles cut into pieces (attn_tc.cu launch_attn_tc)
     peer = comm is not None and comm_kind is not None and comm_kind.startswith("peer")
     scales = 1 if peer else 2
     tail = 0 if comm is None else (2 if peer else 1)

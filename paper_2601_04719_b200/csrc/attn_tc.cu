@@ -116,18 +116,18 @@ struct TcParams {
                          // evict-first loads with normal stores cost ~0.6 GB of extra DRAM reads at C4)
     float *Kh;           // MODE 2: K_hat output [T][D]
     int ngrp;            // work units (groups of CODE_KB K-blocks) per tile row
-    double *split;       // MODE 0, 2: [grid][2][BN][BM] fp64 Delta of tiles split between CTAs (nullptr: MODE 1)
+    double *split;       // MODE 0, 2: [grid][2][BN][BM] fp64 Delta of tiles split between CTAs (nullptr: whole tiles)
+    int pieces;          // pieces per left-over tile (divides ngrp) when split != nullptr
 };
 
 // Work distribution.  A work unit is one group of CODE_KB K-blocks (one accumulator chunk, one code
-// box) of one 128-row tile; units are numbered tile-major.  Every CTA first takes whole tiles in waves
-// (tile b, b + G, ...: the G CTAs stream G adjacent tiles at a time, the write pattern the HBM measured
-// best), then, in modes 0 and 2, an equal contiguous share (to within one unit) of the units of the
-// R = ntiles mod G tiles left over, so that all SMs stream to the end of the pass (with whole tiles
-// only, 512 tiles on 148 SMs run 4 waves, the last 46% full).  A left-over tile whose units fall to two
-// or more CTAs is "split": each CTA holds its piece's Delta in fp64 and writes it to slot 0 (the piece
-// starts inside the tile) or slot 1 (it starts at the tile's first unit), and split_combine_kernel adds
-// the pieces in CTA order and takes |Delta|.  Mode 1 (scores) keeps whole tiles only.
+// box) of one 128-row tile.  Every CTA first takes whole tiles in waves (tile b, b + G, ...: the G CTAs
+// stream G adjacent tiles in lockstep, the write pattern the HBM measured best).  When the R = ntiles mod G
+// tiles left over would leave most SMs idle (R <= G/2), each of them is cut into P equal K-ranges
+// (P | ngrp, R * P <= G) and CTA b takes piece b / R of tile b mod R, so the last wave keeps R * P SMs
+// streaming, still in lockstep.  A cut tile's pieces keep Delta in fp64 and write it to slot 1 (piece 0)
+// or slot 0 (pieces 1..P-1) of their CTA; split_combine_kernel adds the pieces in piece order and takes
+// |Delta|.  Mode 1 (scores) keeps whole tiles only.
 struct Units {
     int n, nfull;              // units of this CTA; whole-tile units among them
     int tail_tile, tail_grp;   // tile and group of the first unit of the tail share
@@ -142,13 +142,16 @@ __device__ __forceinline__ Units make_units(const TcParams &p) {
     if (!p.split) {
         nfull = n = (p.ntiles - b + G - 1) / G * p.ngrp;
     } else {
-        const int64_t W = p.ntiles / G, Ut = (int64_t)(p.ntiles % G) * p.ngrp;
-        const int64_t t0 = Ut * b / G, t1 = Ut * (b + 1) / G;
-        nfull = (int)(W * p.ngrp);
-        n = nfull + (int)(t1 - t0);
-        const int64_t tail0 = W * G * p.ngrp + t0;
-        tt = (int)(tail0 / p.ngrp);
-        tg = (int)(tail0 % p.ngrp);
+        // left-over tile r = b mod R, piece b / R of P: all CTAs of one piece index start at the same
+        // K-block of adjacent tiles (the lockstep the write stream needs; contiguous shares measured slower)
+        const int W = p.ntiles / G, R = p.ntiles - W * G, P = p.pieces, L = p.ngrp / P;
+        nfull = W * p.ngrp;
+        n = nfull;
+        if (b < R * P) {
+            n += L;
+            tt = W * G + b % R;
+            tg = (b / R) * L;
+        }
     }
     Units us;
     us.n = __shfl_sync(0xffffffffu, n, 0);
@@ -245,42 +248,34 @@ __global__ void __launch_bounds__(256) prep_kernel(const float *__restrict__ Q, 
         colq_body(scales, D, nkb, cq, blockIdx.x - nbq, gridDim.x - nbq);
 }
 
-// Split tiles (see make_units): block k < G-1 looks at the boundary between the tail shares of CTAs k
-// and k+1.  If it falls inside a tile and is that tile's first boundary, the block adds the tile's
-// pieces in CTA order (CTA k: slot 1, or slot 0 if its share also started inside the tile; CTAs k+1..:
-// slot 0), takes |Delta| over the tile's rows < T and queries < nq, and writes the sum as partial G + k
-// (zero otherwise).  Fixed order throughout: deterministic.
-constexpr int COMBINE_JQ = 4;  // query quarters per boundary (blockIdx.y): 4x the loads in flight
+// Split tiles (see make_units): block (r, y) adds the P pieces of left-over tile r (CTA pc * R + r holds
+// piece pc: slot 1 for pc = 0, slot 0 otherwise) in piece order for queries [16y, 16y + 16), takes |Delta|
+// over the tile's rows < T and queries < nq, and writes the sum as partial G + r * COMBINE_JQ + y.
+// Fixed order throughout: deterministic.
+constexpr int COMBINE_JQ = 4;  // query quarters per tile (blockIdx.y): 4x the loads in flight
 static_assert(kSplitMaxCtas * (1 + COMBINE_JQ) <= 1024, "partials array: max(num_tiles, 1024) entries");
 __global__ void __launch_bounds__(BM) split_combine_kernel(const double *__restrict__ split, int64_t T, int nq,
-                                                           int64_t ntiles, int ngrp, int G, Partial *partials) {
+                                                           int ntiles, int G, int P, Partial *partials) {
     constexpr int JN = BN / COMBINE_JQ;
-    const int k = blockIdx.x, r = threadIdx.x, j0 = blockIdx.y * JN;
-    const int64_t U = (ntiles % G) * ngrp;  // tail units
-    const int64_t ub = U * (k + 1) / G;      // first tail unit of CTA k+1
-    const int64_t ub_prev = U * k / G;       // first tail unit of CTA k
-    const int64_t tile = ub / ngrp, t0 = tile * ngrp;
+    const int rt = blockIdx.x, r = threadIdx.x, j0 = blockIdx.y * JN;
+    const int W = ntiles / G, R = ntiles - W * G;
     pdl_wait();  // the pieces written by the tensor-core pass
     pdl_trigger();
-    double attn = 0.0;
-    if (ub % ngrp != 0 && ub_prev <= t0) {
-        const int64_t row = ((ntiles / G) * G + tile) * BM + r;
-        double d[JN];
+    const int64_t row = ((int64_t)W * G + rt) * BM + r;
+    double d[JN];
 #pragma unroll
-        for (int j = 0; j < JN; j++) d[j] = 0.0;
-        for (int c = k; c < G && U * c / G < t0 + ngrp; c++) {
-            if (U * (c + 1) / G == U * c / G) continue;  // empty tail share: no piece
-            const int slot = (U * c / G > t0) ? 0 : 1;
-            const double *sp = split + ((int64_t)c * 2 + slot) * (BN * BM) + (int64_t)j0 * BM;
+    for (int j = 0; j < JN; j++) d[j] = 0.0;
+    for (int pc = 0; pc < P; pc++) {
+        const double *sp = split + ((int64_t)(pc * R + rt) * 2 + (pc > 0 ? 0 : 1)) * (BN * BM) + (int64_t)j0 * BM;
 #pragma unroll
-            for (int j = 0; j < JN; j++)
-                if (j0 + j < nq) d[j] += sp[j * BM + r];
-        }
-        if (row < T)
-#pragma unroll
-            for (int j = 0; j < JN; j++)
-                if (j0 + j < nq) attn += fabs(d[j]);
+        for (int j = 0; j < JN; j++)
+            if (j0 + j < nq) d[j] += sp[j * BM + r];
     }
+    double attn = 0.0;
+    if (row < T)
+#pragma unroll
+        for (int j = 0; j < JN; j++)
+            if (j0 + j < nq) attn += fabs(d[j]);
     __shared__ double red[BM];
     red[r] = attn;
     __syncthreads();
@@ -288,7 +283,7 @@ __global__ void __launch_bounds__(BM) split_combine_kernel(const double *__restr
         if (r < o) red[r] += red[r + o];
         __syncthreads();
     }
-    if (r == 0) partials[G + k * COMBINE_JQ + blockIdx.y] = Partial{0.0, red[0], 0.0, 0.0};
+    if (r == 0) partials[G + rt * COMBINE_JQ + blockIdx.y] = Partial{0.0, red[0], 0.0, 0.0};
 }
 
 // byte address of 16-byte chunk c of row r in a [rows][128 B] tile with the TMA 128B swizzle
@@ -777,21 +772,24 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
         p.Kh = Kh_out;
     }
     p.ngrp = (int)((nkb + CODE_KB - 1) / CODE_KB);
-    const int64_t nunits = (int64_t)ntiles * p.ngrp;
     // modes 0/2: whole-tile waves + balanced tail (tiles may be split, see make_units); mode 1: whole tiles
-    // Balanced tail only where whole tiles leave the last wave less than 60% full after at least one
-    // full wave (the C4 shard at 2 ranks: 512 tiles on 148 SMs = 3 waves + 46%; measured 0.98 vs
-    // 1.03 ms).  One wave (the 128 tiles of a C4 shard at 8 ranks), 1.73 waves (4 ranks: balanced
-    // measured 2% slower) and 6.9 waves (C4 on one GPU) stay whole.
+    // Cut left-over tiles only where whole tiles leave the last wave at most half full after at least one
+    // full wave (the C4 shard at 2 ranks: 512 tiles on 148 SMs = 3 waves + 68 tiles -> 2 pieces each).  One
+    // wave (the 128 tiles of a C4 shard at 8 ranks) and fuller last waves stay whole.
     const int nsm = std::min(device_info().num_sms, kSplitMaxCtas);
-    const int64_t last = ntiles % nsm;  // tiles in the partial last wave
-    const char *force = std::getenv("KVQ_TC_BALANCE");  // experiments: 0 = whole tiles, 1 = balanced tail
-    const bool want = force ? force[0] == '1' : (ntiles > nsm && last > 0 && last * 10 < nsm * 6);
-    const bool balanced = mode != 1 && ws_split != nullptr && want;
-    const int grid = !balanced ? std::min(ntiles, device_info().num_sms) : (int)std::min<int64_t>(nunits, nsm);
+    const int W0 = ntiles / nsm, R0 = W0 ? ntiles % nsm : ntiles;
+    int P = 1;
+    for (int c = 2; R0 > 0 && c <= p.ngrp && R0 * c <= nsm; c++)
+        if (p.ngrp % c == 0) P = c;
+    const char *force = std::getenv("KVQ_TC_BALANCE");  // experiments: 0 = whole tiles, 1 = cut whenever P >= 2
+    const bool want = force ? force[0] == '1' : W0 >= 1;
+    const bool balanced = mode != 1 && ws_split != nullptr && want && P >= 2;
+    const int grid = !balanced ? std::min(ntiles, device_info().num_sms) : (W0 ? nsm : R0 * P);
     p.split = balanced ? reinterpret_cast<double *>(ws_split) : nullptr;
+    p.pieces = balanced ? P : 1;
+    const int R = balanced ? ntiles - (ntiles / grid) * grid : 0;
     const size_t smem = sizeof(Smem);
-    if (grid_out) *grid_out = balanced ? grid + COMBINE_JQ * (grid - 1) : grid;  // + per CTA boundary and quarter
+    if (grid_out) *grid_out = balanced ? grid + COMBINE_JQ * R : grid;  // + one partial per cut tile and quarter
     if (mode == 0)
         launch_mode<0>(mK, mKh, mKq, p, grid, smem, s);
     else if (mode == 1)
@@ -799,10 +797,10 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
     else
         launch_mode<2>(mK, mKh, mKq, p, grid, smem, s);
     if (kvq_status st = check_launch(mode == 0 ? "attn_tc(metrics)" : mode == 1 ? "attn_tc(scores)" : "attn_tc(roundtrip)");
-        st != KVQ_OK || !balanced || grid == 1)
+        st != KVQ_OK || !balanced || R == 0)
         return st;
-    (void)launch_pdl(split_combine_kernel, dim3(grid - 1, COMBINE_JQ), dim3(BM), 0, s, (const double *)p.split, T,
-                     (int)nq, (int64_t)ntiles, p.ngrp, grid, reinterpret_cast<Partial *>(partials));
+    (void)launch_pdl(split_combine_kernel, dim3(R, COMBINE_JQ), dim3(BM), 0, s, (const double *)p.split, T, (int)nq,
+                     ntiles, grid, P, reinterpret_cast<Partial *>(partials));
     return check_launch("attn_tc(split_combine)");
 }
 
