@@ -13,6 +13,8 @@ N ranks (strong scaling).  Rank 0 prints one JSON line.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1..C4] [--impl kvq|reference]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+`--gpus N` (N > 1) without torchrun re-launches itself under torch.distributed.run with N processes
+(one per GPU) and exits non-zero when fewer than N GPUs are visible.
 """
 from __future__ import annotations
 
@@ -35,6 +37,7 @@ CONFIGS = {  # BASELINE.json configs
 }
 METRIC = "quantize+dequantize elements/s and achieved HBM GB/s vs B200 peak at 1/2/4/8 GPUs"
 # Algorithmic bytes per element of each pass: what the method itself must move.
+SPIN_CYCLES = 100_000  # ~50 us device spin queued ahead of each timed step (keeps launch latency out)
 BYTES = {"scales": 4, "quantize": 5, "dequantize": 5, "metrics": 8, "roundtrip": 9, "quantize_dequantize_e4m3": 9,
          "quantize_dequantize_int4": 8.5, "quantize_dequantize_int2": 8.25}
 
@@ -127,21 +130,47 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle (baseline / reference arm)
+ORACLE_PASSES = ("scales", "quantize", "dequantize", "recon_errors", "attention")
+
+
 def oracle_step(cfg, rows: int):
-    """The oracle as it stands on the first `rows` rows of the workload:
-    scales + quantize + dequantize + L2/max + attention error (nq queries).
-    Returns (seconds, elements).  Generation is excluded."""
+    """The oracle as it stands on the first `rows` rows of the workload, one pass at a time:
+    scales (a1+a2), quantize (a3), dequantize (a4), L2/max-abs (a5), attention error (a6, nq queries).
+    Returns ({pass: seconds}, elements).  Generation is excluded."""
     import oracle
     D, nq = cfg["D"], cfg["nq"]
     K = oracle.fill(rows, D, oracle.SEED_K)
     Q = oracle.fill(nq, D, oracle.SEED_Q)
+    t = {}
     t0 = time.perf_counter()
     s = oracle.compute_scales(K)
+    t1 = time.perf_counter()
     q = oracle.quantize(K, s)
+    t2 = time.perf_counter()
     Kh = oracle.dequantize(q, s)
+    t3 = time.perf_counter()
     oracle.recon_errors(K, Kh)
+    t4 = time.perf_counter()
     oracle.attention_abs_sum(Q, K, Kh)
-    return time.perf_counter() - t0, rows * D
+    t5 = time.perf_counter()
+    t = dict(zip(ORACLE_PASSES, (t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4)))
+    return t, rows * D
+
+
+def qdq_seconds(t: dict) -> float:
+    """The metric's own mix (quantize+dequantize elements/s): scales + quantize + dequantize."""
+    return t["scales"] + t["quantize"] + t["dequantize"]
+
+
+def cpu_report(t: dict, n: int, steps: int = 1) -> dict:
+    """Per-pass oracle seconds and elements/s of the metric's mix (value) and of the whole step."""
+    full = sum(t.values())
+    return {"value": n * steps / qdq_seconds(t), "unit": "elements/s",
+            "per_pass_s": {k: v / steps for k, v in t.items()},
+            "per_pass_elements_per_s": {k: n * steps / v for k, v in t.items() if v > 0},
+            "full_step_elements_per_s": n * steps / full,
+            "value_mix": "scales+quantize+dequantize (a1-a4, the metric's quantize+dequantize); "
+                         "full_step_elements_per_s adds a5 L2/max and a6 attention (the GPU step's remaining work)"}
 
 
 def host_info() -> dict:
@@ -178,32 +207,35 @@ class one_core:
 
 def oracle_rows_for(cfg, seconds: float) -> int:
     t, n = oracle_step(cfg, 8)
-    per_row = t / 8
+    per_row = sum(t.values()) / 8
     return max(8, min(cfg["T"], int(seconds / per_row)))
 
 
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the oracle (plain C, single thread) is this tier's reference arm."""
+    """--impl reference: the oracle (plain C, single thread) is this tier's reference arm.
+    Under torchrun only rank 0 works; the others exit 0 at once."""
     if rank != 0:
         return
     rows = oracle_rows_for(cfg, 0.5 if args.steps * 1 <= 200 else 0.2)
     for _ in range(args.warmup):
         oracle_step(cfg, rows)
-    ts = []
+    tot = dict.fromkeys(ORACLE_PASSES, 0.0)
     with one_core():
         for _ in range(args.steps):
             t, n = oracle_step(cfg, rows)
-            ts.append(t)
-    tot = sum(ts)
-    value = rows * cfg["D"] * args.steps / tot
-    sample = f"first {rows} rows of {cfg['name']} ({rows}x{cfg['D']} elements) per step, nq={cfg['nq']}"
+            for k in tot:
+                tot[k] += t[k]
+    rep = cpu_report(tot, rows * cfg["D"], args.steps)
+    value = rep["value"]
+    ms = 1e3 * qdq_seconds(tot) / args.steps
+    sample = (f"first {rows} rows of {cfg['name']} ({rows}x{cfg['D']} elements) per step; value = scales+quantize"
+              f"+dequantize, per-pass seconds include L2/max and attention (nq={cfg['nq']})")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (splitmix64 lattice uniform [-1,1), SURVEY §8(d))",
             "config": {"workload": f"{cfg['name']}: {cfg['desc']}", "T": cfg["T"], "D": cfg["D"], "nq": cfg["nq"]},
-            "cpu_baseline": {"value": value, "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": sample,
-                             **host_info()},
+            "cpu_baseline": {**rep, "cores": 1, "kind": "oracle", "sample": sample, **host_info()},
             "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -239,7 +271,7 @@ def run_kvq(args, cfg, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2601_04719_b200 import kvq
-    from paper_2601_04719_b200.dist import make_comm, make_peer, max_over_ranks, shard_rows
+    from paper_2601_04719_b200.dist import make_comm, make_peer, max_over_ranks, max_over_ranks_vec, shard_rows
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -352,23 +384,41 @@ def run_kvq(args, cfg, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # Per-step timing: before every step a barrier (N > 1) and a device sync; then a short
+    # device-side spin (torch.cuda._sleep) is queued ahead of the step so the host enqueues all of the step's
+    # launches while the stream is still busy (launch latency stays outside the events, as in back-to-back
+    # steps).  Each rank times its own step with CUDA events on the launching stream; the step time is the
+    # max over ranks, per step; ms_per_step is the median of those, min and mean are reported beside it.
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    se = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local_rank) as clk:
         wall0 = time.time()
-        start.record(stream)
         for i in range(args.steps):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            torch.cuda._sleep(SPIN_CYCLES)
+            se[i][0].record(stream)
             step(evs[i] if args.pass_events else None)
-        end.record(stream)
+            se[i][1].record(stream)
         torch.cuda.synchronize()
         wall1 = time.time()
     if world > 1:
         dist.barrier()
-    ms_local = start.elapsed_time(end) / args.steps
-    ms = max_over_ranks(ms_local, dev if world > 1 else None)
+    per_step = [a.elapsed_time(b) for a, b in se]
+    per_step = max_over_ranks_vec(per_step, dev if world > 1 else None)
+    ms = statistics.median(per_step)
+    # the same steps back to back (no sync between them), for context
+    b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    b0.record(stream)
+    for i in range(args.steps):
+        step()
+    b1.record(stream)
+    torch.cuda.synchronize()
+    ms_b2b = max_over_ranks(b0.elapsed_time(b1) / args.steps, dev if world > 1 else None)
     metrics = kvq.metrics_from_device(mout)
 
     # per-pass device time (events on the launching stream), averaged over the timed steps
@@ -473,13 +523,18 @@ def run_kvq(args, cfg, rank, world, local_rank):
         with one_core():
             rows_cpu = oracle_rows_for(cfg, args.cpu_seconds)
             t_cpu, n_cpu = oracle_step(cfg, rows_cpu)
-        cpu = {"value": n_cpu / t_cpu, "unit": "elements/s", "cores": 1, "kind": "oracle",
-               "sample": f"first {rows_cpu} rows of {cfg['name']} ({n_cpu} elements): scales+quantize+dequantize"
-                         f"+L2/max+attention(nq={nq}), plain C single thread pinned to one core, generation excluded",
-               "seconds": t_cpu, **host_info()}
+        cpu = {**cpu_report(t_cpu, n_cpu), "cores": 1, "kind": "oracle",
+               "sample": f"first {rows_cpu} rows of {cfg['name']} ({n_cpu} elements), each pass timed alone: "
+                         f"scales, quantize, dequantize, L2/max, attention (nq={nq}); plain C single thread "
+                         f"pinned to one core, generation excluded",
+               "seconds": sum(t_cpu.values()), **host_info()}
     line = {
         "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms, "ms_min": min(per_step), "ms_mean": statistics.mean(per_step),
+        "ms_back_to_back": ms_b2b,
+        "timing": "per step: barrier + device sync, CUDA events on the launching stream, max over ranks; "
+                  "ms_per_step = median over steps",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (splitmix64 lattice uniform [-1,1), SURVEY §8(d))",
         "config": {"workload": f"{cfg['name']}: {cfg['desc']}", "T": T, "D": D, "nq": nq,
                    "step": ("kvq_compute_scales_fmt(E4M3) -> kvq_quantize_e4m3(+K_hat) -> kvq_error_metrics_async"
@@ -501,6 +556,27 @@ def run_kvq(args, cfg, rank, world, local_rank):
         "fidelity": {k: metrics[k] for k in ("l2", "max_abs", "attn_mean_abs", "theoretical_max")},
     }
     print(json.dumps(line), flush=True)
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(n: int, argv: list, device_count=None, run=subprocess.call) -> int:
+    """`python bench.py --gpus N` without torchrun: one process per GPU under torch.distributed.run (the
+    driver's own launch line), after checking that N GPUs are visible.  Never falls back to fewer GPUs."""
+    if device_count is None:
+        import torch
+        device_count = torch.cuda.device_count()
+    if device_count < n:
+        print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {device_count}", file=sys.stderr, flush=True)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
+    return run(cmd)
 
 
 def main():
@@ -532,6 +608,10 @@ def main():
         run_reference(args, cfg, rank, world)
         return
     launched = "WORLD_SIZE" in os.environ  # torchrun / torch.distributed.run
+    if not launched and args.gpus > 1:
+        sys.exit(self_launch(args.gpus, sys.argv[1:]))
+    if launched and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one process per GPU")
     if launched:
         import torch
         import torch.distributed as dist

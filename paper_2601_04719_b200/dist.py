@@ -38,6 +38,16 @@ def max_over_ranks(x: float, device=None) -> float:
     return float(t.item())
 
 
+def max_over_ranks_vec(xs, device=None) -> list:
+    """Element-wise max over all ranks of a per-rank list of scalars (per-step device times)."""
+    xs = [float(x) for x in xs]
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return xs
+    t = torch.tensor(xs, dtype=torch.float64, device=device or "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
+
 def sum_over_ranks(x: float, device=None) -> float:
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
         return float(x)

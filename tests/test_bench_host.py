@@ -49,3 +49,40 @@ def test_separate_and_format_launch_counts(bench, b200):
     assert bench.launches_per_step(args(pipeline="separate"), None, None, 131072, 8192) == 7
     # scales (2) + the format's fused quantize+dequantize + metrics (3)
     assert bench.launches_per_step(args(fmt="e4m3"), None, None, 131072, 8192) == 6
+
+
+def test_gpus_n_self_launches_under_torchrun(bench):
+    """`bench.py --gpus 2` without torchrun re-launches itself with 2 processes (never a silent 1-GPU run)."""
+    seen = []
+    rc = bench.self_launch(2, ["--gpus", "2", "--steps", "3"], device_count=8, run=lambda c: seen.append(c) or 0)
+    assert rc == 0 and len(seen) == 1
+    cmd = seen[0]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=2" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[-3:] == ["--gpus", "2", "--steps", "3"][-3:] and cmd[-4] == "--gpus"
+
+
+def test_gpus_n_fails_loudly_without_enough_gpus(bench, capsys):
+    rc = bench.self_launch(4, ["--gpus", "4"], device_count=1, run=lambda c: pytest.fail("must not launch"))
+    assert rc != 0
+    assert "needs 4 visible GPUs, found 1" in capsys.readouterr().err
+
+
+def test_gpus_n_cli_exits_nonzero_on_cpu_box():
+    """End to end through the CLI on this GPU-less box: exit code != 0 and no JSON line claiming n_gpus 1."""
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode != 0
+    assert '"n_gpus"' not in r.stdout
+
+
+def test_cpu_report_per_pass(bench):
+    t = {"scales": 1.0, "quantize": 2.0, "dequantize": 1.0, "recon_errors": 1.0, "attention": 5.0}
+    r = bench.cpu_report(t, 400, steps=2)
+    assert r["value"] == 400 * 2 / 4.0
+    assert r["full_step_elements_per_s"] == 400 * 2 / 10.0
+    assert r["per_pass_s"]["attention"] == 2.5
