@@ -37,6 +37,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "device_common.cuh"
 #include "kvq_internal.h"
@@ -61,24 +62,53 @@ struct Ring {
 // warps: 0 K producer, 1 MMA (+TMEM alloc), 2 output stores (fused mode), 3 Q producer, 4-11 converters (2 per TMEM lane
 // quarter, 16 columns each), 12-15 epilogue.  Warpgroup 0 gives registers to the
 // epilogue warpgroup (setmaxnreg), which keeps 64 fp64 accumulators per row.
-constexpr int NTHREADS = 512;
-constexpr int NCONV = 256;  // converter threads
-constexpr int CONV_W0 = 4, EPI_W0 = 12;
+#ifndef KVQ_TC_TEAMS
+#define KVQ_TC_TEAMS 2
+#endif
+constexpr int NTEAMS = KVQ_TC_TEAMS;  // converter teams; team t converts the K-blocks g with g % NTEAMS == t
+constexpr int NCONV = 256;            // converter threads per team
+constexpr int NCONV_W = NCONV / 32;   // converter warps per team (one elected arrival per warp after __syncwarp)
+constexpr int CONV_W0 = 4, EPI_W0 = CONV_W0 + NTEAMS * NCONV_W;
+constexpr int NTHREADS = (EPI_W0 + 4) * 32;
+// setmaxnreg budgets (64K registers per SM): warpgroup 0 (single-lane roles) and the epilogue warpgroup
+// (setmaxnreg only moves registers within the CTA's launch allocation: NTHREADS x the launch count)
+constexpr uint32_t REG_LAUNCH = 65536 / NTHREADS / 8 * 8;
+constexpr uint32_t REG_WG0 = NTEAMS == 1 ? 56 : 48, REG_EPI = NTEAMS == 1 ? 200 : 80;
+constexpr uint32_t REG_CONV = NTEAMS == 1 ? 128 : (REG_LAUNCH * (NTHREADS / 128) - REG_WG0 - REG_EPI) / (NTEAMS * 2) / 8 * 8;
+static_assert(REG_WG0 + REG_EPI + REG_CONV * NTEAMS * 2 <= REG_LAUNCH * (NTHREADS / 128), "register budget");
 constexpr int CHUNK_KB = 4;              // K-blocks (of 32 columns) per TMEM accumulation chunk
 constexpr int CODE_KB = 4;               // K-blocks per code store (128 codes = one 128 B line per row)
 constexpr uint32_t KTILE = BM * BK * 4;  // 16 KB
 constexpr uint32_t QTILE = BN * BK * 4;  // 8 KB (one of hi/lo)
 constexpr uint32_t TMEM_COLS = 512;      // acc 2 x 64 | A ring AST x (hi 32 + lo 32) (| 128 spare)
 constexpr uint32_t A_COL0 = 128;
+constexpr uint32_t ACC_COL0 = 384;       // two converter teams: the tile's Delta as fp32 (hi, lo) pairs (2 x 64 columns)
 constexpr uint32_t IDESC = idesc_tf32(BM, BN);
 
-// Per K-block quantizer record (fused mode): {s, RN(1/s)} of the 32 columns and a
+// Per K-block quantizer record (fused mode): RN(1/s) and s of the 32 columns (as two arrays, so that
+// adjacent columns form the fp32 pairs of the packed arithmetic) and a
 // flag set when one of them needs the exact path for every element.
 struct __align__(16) ColRec {
-    float2 c[BK];
+    float y[BK];  // RN(1/s) per column (0: zero scale or exact path)
+    float s[BK];  // s per column
     uint32_t any_exact;
     uint32_t pad[3];
 };
+
+// Timeline trace of CTA 0 (experiments only, -DKVQ_TRACE): clock64 of event e at K-block g in [TR_G0, TR_G0 + TR_N).
+#ifdef KVQ_TRACE
+constexpr int TR_G0 = 64, TR_N = 64, TR_E = 16;
+__device__ unsigned long long g_kvq_trace[TR_N][TR_E];
+#define KVQ_TR(e, cond)                                                                            \
+    do {                                                                                           \
+        if ((cond) && blockIdx.x == 0 && (int)g >= TR_G0 && (int)g < TR_G0 + TR_N)                 \
+            g_kvq_trace[g - TR_G0][e] = clock64();                                                 \
+    } while (0)
+#else
+#define KVQ_TR(e, cond) \
+    do {                \
+    } while (0)
+#endif
 
 // Waits on the critical path (MMA issuer, converters): a tight try_wait loop, or
 // the hardware-suspending variant when built with -DKVQ_SLEEP_ALL.
@@ -100,7 +130,7 @@ struct __align__(1024) Smem {
     uint64_t full_a[AST], empty_a[AST], full_acc[2], empty_acc[2];
     uint64_t staged[KST_MAX], cstored[2];  // fused mode: handoff converters -> store warp -> converters
     uint32_t tmem_base;
-    double red[3][8];
+    double red[3][NTEAMS * 8];
 };
 
 static_assert(sizeof(Smem) <= 227 * 1024, "shared memory budget (227 KB per CTA on sm_100)");
@@ -226,7 +256,8 @@ __device__ __forceinline__ void colq_body(const float *__restrict__ scales, int6
         const int64_t d = kb * BK + lx;
         const float sd = d < D ? scales[d] : 0.0f;
         const ColQ c = make_colq(sd);
-        out[kb].c[lx] = make_float2(sd, c.y);
+        out[kb].y[lx] = c.y;
+        out[kb].s[lx] = sd;
         const unsigned any = __ballot_sync(0xffffffffu, c.exact);
         if (lx == 0) {
             out[kb].any_exact = any ? 1u : 0u;
@@ -309,15 +340,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (smem_u32(smem_raw) & 1023u) __trap();  // swizzle atoms need 1024-byte alignment
         for (int i = 0; i < Ring<MODE>::kst; i++) {
             mbar_init(&s.full_k[i], 1);
-            mbar_init(&s.empty_k[i], MODE == 2 ? 1 : NCONV);  // fused: the store warp frees the stage
-            mbar_init(&s.staged[i], NCONV);
+            mbar_init(&s.empty_k[i], MODE == 2 ? 1 : NCONV_W);  // fused: the store warp frees the stage
+            mbar_init(&s.staged[i], NCONV_W);
         }
         for (int i = 0; i < QST; i++) {
             mbar_init(&s.full_q[i], 1);
             mbar_init(&s.empty_q[i], 1);
         }
         for (int i = 0; i < AST; i++) {
-            mbar_init(&s.full_a[i], NCONV);
+            mbar_init(&s.full_a[i], NCONV_W);
             mbar_init(&s.empty_a[i], 1);
         }
         for (int i = 0; i < 2; i++) {
@@ -345,7 +376,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const Units us = make_units(p);
 
     if (warp < CONV_W0) {
-        setmaxnreg_dec<56>();  // warpgroup 0: producer + MMA issuer need few registers
+        setmaxnreg_dec<REG_WG0>();  // warpgroup 0: producer + MMA issuer need few registers
         if (warp == 0 && lane == 0) {
             // ------------------------------------------------------------ producer
             const uint64_t pol_stream = (p.hints & 1) ? policy_evict_first() : policy_evict_normal();
@@ -358,6 +389,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int kb = kb0; kb < kb1; kb++, g++) {
                     const int sk = g % KST;
                     mbar_wait_sleep(&s.empty_k[sk], ((g / KST) & 1) ^ 1);
+                    KVQ_TR(0, true);
                     mbar_arrive_tx(&s.full_k[sk], kbytes);
                     uint8_t *stg = s.buf + sk * Ring<MODE>::stage;
                     tma_load_2d(stg, &tmK, &s.full_k[sk], kb * BK, tile * BM, pol_stream);
@@ -396,14 +428,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int kb = kb0; kb < kb1; kb++, g++) {
                     const int sk = g % KST;
                     mbar_wait_sleep(&s.staged[sk], (g / KST) & 1);
+                    KVQ_TR(7, true);
+#ifndef KVQ_EXP_NOSTORE  // timing experiments only (outputs not written)
                     tma_store_2d(&tmKh, s.buf + sk * Ring<MODE>::stage, kb * BK, tile * BM, pol_out);
+#endif
                     const bool group_end = kb == kb1 - 1;
+#ifndef KVQ_EXP_NOSTORE
                     if (group_end)
+#else
+                    if (false)
+#endif
                         tma_store_2d(&tmKq, s.buf + 128 * 1024 + (grp & 1) * KTILE, (kb / CODE_KB) * (BK * CODE_KB),
                                      tile * BM, pol_out);
                     bulk_commit();
                     if (g > 0) {
                         bulk_wait_read<1>();  // block g-1's boxes have left smem
+                        KVQ_TR(8, true);
                         mbar_arrive(&s.empty_k[(g - 1) % KST]);
                         if (prev_group_end) mbar_arrive(&s.cstored[(grp - 1) & 1]);
                     }
@@ -412,8 +452,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
             bulk_wait<0>();  // all K_hat / code writes complete before the CTA retires
-        } else if (warp == 1 && lane == 0) {
+        } else if (warp == 1) {
             // ------------------------------------------------------------ MMA issuer
+            // The whole warp walks the loop and waits (loop state and descriptors are warp-uniform, so they
+            // live in uniform registers); one elected lane issues the MMAs and commits.  (A single-lane role
+            // issues each tcgen05.mma through a per-instruction uniformization loop: ~1000 cycles per K-block.)
             uint32_t g = 0, gc = 0;
             for (UnitWalk w(us); w.ok(); w.next()) {
                 const int kb0 = w.grp * CODE_KB, kb1 = min(kb0 + CODE_KB, nkb);
@@ -429,33 +472,40 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                     const int sa = g % AST, sq = g % QST;
                     KVQ_WAIT_HOT(&s.full_a[sa], (g / AST) & 1);
+                    KVQ_TR(9, lane == 0);
                     KVQ_WAIT_HOT(&s.full_q[sq], (g / QST) & 1);
                     tc_fence_after();
                     const uint32_t ahi = tbase + A_COL0 + sa * 64, alo = ahi + 32;
-                    const uint32_t qhi = smem_u32(s.q[sq]), qlo = qhi + QTILE;
+                    const uint32_t qhi = smem_u32(s.q[sq]);
+                    // K-step j covers k-groups 2j, 2j+1 (LBO apart = 1024 B), 8-row groups 128 B apart;
+                    // step j starts 2048 B further (+128 in the descriptor's 16-byte address field)
+                    const uint64_t bh0 = smem_desc(qhi, 1024, 128), bl0 = smem_desc(qhi + QTILE, 1024, 128);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int j = 0; j < BK / 8; j++) {
-                        // K-step j covers k-groups 2j, 2j+1 (LBO apart = 1024 B), 8-row groups 128 B apart
-                        const uint64_t bh = smem_desc(qhi + j * 2048, 1024, 128);
-                        const uint64_t bl = smem_desc(qlo + j * 2048, 1024, 128);
-                        mma_tf32_ts(d, ahi + 8 * j, bh, IDESC, (!chunk_first || j != 0) ? 1u : 0u);
-                        mma_tf32_ts(d, ahi + 8 * j, bl, IDESC, 1);
-                        mma_tf32_ts(d, alo + 8 * j, bh, IDESC, 1);
+                        for (int j = 0; j < BK / 8; j++) {
+#ifndef KVQ_EXP_NOMMA  // timing experiments only (Delta not computed)
+                            mma_tf32_ts(d, ahi + 8 * j, bh0 + 128u * j, IDESC, (!chunk_first || j != 0) ? 1u : 0u);
+                            mma_tf32_ts(d, ahi + 8 * j, bl0 + 128u * j, IDESC, 1);
+                            mma_tf32_ts(d, alo + 8 * j, bh0 + 128u * j, IDESC, 1);
+#endif
+                        }
+                        mma_commit(&s.empty_a[sa]);
+                        mma_commit(&s.empty_q[sq]);
+                        if (chunk_last) mma_commit(&s.full_acc[ab]);
                     }
-                    mma_commit(&s.empty_a[sa]);
-                    mma_commit(&s.empty_q[sq]);
-                    if (chunk_last) {
-                        mma_commit(&s.full_acc[ab]);
-                        gc++;
-                    }
+                    __syncwarp();
+                    KVQ_TR(10, lane == 0);
+                    if (chunk_last) gc++;
                 }
             }
         }
     } else if (warp < EPI_W0) {
         // ------------------------------------------------------------ converters (warps 4..11)
         // thread = (row r, half h): columns 16h..16h+15 of every 32-column K-block
+        if constexpr (REG_CONV > REG_LAUNCH) setmaxnreg_inc<REG_CONV>();
+        const int team = (warp - CONV_W0) / NCONV_W;
         const int quarter = warp & 3;
-        const int h = (warp - CONV_W0) >> 2;
+        const int h = ((warp - CONV_W0) % NCONV_W) >> 2;
         const int r = quarter * 32 + lane;  // row of the tile == TMEM lane
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         double ss = 0.0;
@@ -463,12 +513,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         uint32_t g = 0, cgrp = 0;  // K-block and code-group counters (same order as the store warp)
         for (UnitWalk w(us); w.ok(); w.next()) {
             const int kb0 = w.grp * CODE_KB, kb1 = min(kb0 + CODE_KB, nkb);
+            bool code_buf_ready = false;  // this team has waited for the group's code buffer
             #pragma unroll 1
             for (int kb = kb0; kb < kb1; kb++, g++) {
+                if (NTEAMS > 1 && (int)(g % NTEAMS) != team) {  // the other team's K-block
+                    if (kb == kb1 - 1) cgrp++;
+                    continue;
+                }
                 const int sk = g % KST;
+                KVQ_TR(14, lane == 0 && warp == CONV_W0);
                 KVQ_WAIT_HOT(&s.full_k[sk], (g / KST) & 1);
+                KVQ_TR(1, lane == 0 && warp == CONV_W0); KVQ_TR(5, lane == 0 && warp == EPI_W0 - 1);
                 const uint32_t kbase = smem_u32(s.buf + sk * Ring<MODE>::stage);
-                float e[16];
+                uint64_t E[8];  // E = K - K_hat as fp32 pairs (columns 2j, 2j+1 of this thread's 16)
                 if (MODE != 2) {
                     const uint32_t hbase = kbase + KTILE;
 #pragma unroll
@@ -476,102 +533,131 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         const float4 a = lds128(swz(kbase, r, 4 * h + c));
                         float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
                         if (has_khat) b = lds128(swz(hbase, r, 4 * h + c));
-                        e[4 * c + 0] = __fsub_rn(a.x, b.x);
-                        e[4 * c + 1] = __fsub_rn(a.y, b.y);
-                        e[4 * c + 2] = __fsub_rn(a.z, b.z);
-                        e[4 * c + 3] = __fsub_rn(a.w, b.w);
+                        E[2 * c] = f2sub(f2pk(a.x, a.y), f2pk(b.x, b.y));
+                        E[2 * c + 1] = f2sub(f2pk(a.z, a.w), f2pk(b.z, b.w));
                     }
-                    mbar_arrive(&s.empty_k[sk]);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&s.empty_k[sk]);
                 } else {
                     // ---- a3 + a4 on the resident K row segment (Eq. 7, Eq. 8); same arithmetic and
-                    // exactness argument as quant_v4_kernel (device_common.cuh)
-                    float x[16], v[16], xh[16];
+                    // exactness argument as quant_v4_kernel (device_common.cuh), two columns per
+                    // instruction (FMUL2/FADD2: each lane the IEEE RN operation of the scalar code).
+                    // The clamp to +-127 is folded into the repair test: for a scale formed from the
+                    // column's own maximum (Eq. 6) |fq| <= 127 (1 + 2^-22), so |fq| > 127.25 only happens
+                    // for caller scales below max/127 and sends the segment to the exact path below.
+                    uint64_t X[8], V[8], XH[8];
 #pragma unroll
                     for (int c = 0; c < 4; c++) {
                         const float4 a = lds128(swz(kbase, r, 4 * h + c));
-                        x[4 * c + 0] = a.x;
-                        x[4 * c + 1] = a.y;
-                        x[4 * c + 2] = a.z;
-                        x[4 * c + 3] = a.w;
+                        X[2 * c] = f2pk(a.x, a.y);
+                        X[2 * c + 1] = f2pk(a.z, a.w);
                     }
-                    const uint32_t cqb = smem_u32(&s.cq[sk]) + 16 * h * 8;  // this half's 16 {s, y}
-                    float dmax = 0.0f;
+                    const uint32_t cyb = smem_u32(&s.cq[sk]) + 64 * h;  // y[16h .. 16h+15], then s[...] at +128
+                    const uint64_t M2 = f2pk(kMagic, kMagic);
+                    float amax = 0.0f, dmax = 0.0f;
 #pragma unroll
-                    for (int c2 = 0; c2 < 8; c2++) {
-                        const float4 cq = lds128(cqb + 16 * c2);  // {s, y} of 2 columns (broadcast read)
+                    for (int c = 0; c < 4; c++) {
+                        const float4 y4 = lds128(cyb + 16 * c);        // broadcast reads
+                        const float4 s4 = lds128(cyb + 128 + 16 * c);
 #pragma unroll
                         for (int u = 0; u < 2; u++) {
-                            const int i = 2 * c2 + u;
-                            const float sc = u ? cq.z : cq.x, y = u ? cq.w : cq.y;
-                            const float cl = fminf(fmaxf(__fmul_rn(x[i], y), -127.0f), 127.0f);
-                            const float vv = __fadd_rn(cl, kMagic);
-                            const float rr = __fsub_rn(vv, kMagic);
-                            dmax = fmaxf(dmax, fabsf(__fsub_rn(cl, rr)));
-                            v[i] = vv;
-                            xh[i] = __fmul_rn(rr, sc);
+                            const int j = 2 * c + u;
+                            const uint64_t fq = f2mul(X[j], u ? f2pk(y4.z, y4.w) : f2pk(y4.x, y4.y));
+                            const uint64_t vv = f2add(fq, M2);
+                            const uint64_t rr = f2sub(vv, M2);
+                            const uint64_t dd = f2sub(fq, rr);
+                            amax = fmaxf(amax, fmaxf(fabsf(f2lo(fq)), fabsf(f2hi(fq))));
+                            dmax = fmaxf(dmax, fmaxf(fabsf(f2lo(dd)), fabsf(f2hi(dd))));
+                            V[j] = vv;
+                            XH[j] = f2mul(rr, u ? f2pk(s4.z, s4.w) : f2pk(s4.x, s4.y));
                         }
                     }
-                    if (dmax > kDangerThr || s.cq[sk].any_exact) {
-                        // rare: a near-tie quotient or an exact-path column -> IEEE division there
+                    if (dmax > kDangerThr || amax > 127.25f || s.cq[sk].any_exact) {
+                        // rare: a near-tie quotient, a quotient past the clamp or an exact-path column ->
+                        // the whole segment again with the clamp and, where needed, the IEEE division
 #pragma unroll
                         for (int i = 0; i < 16; i++) {
-                            const float2 cy = s.cq[sk].c[16 * h + i];
-                            const float cl = fminf(fmaxf(__fmul_rn(x[i], cy.y), -127.0f), 127.0f);
-                            const float rr = __fsub_rn(__fadd_rn(cl, kMagic), kMagic);
-                            if (fabsf(__fsub_rn(cl, rr)) > kDangerThr || (cy.y == 0.0f && cy.x != 0.0f)) {
-                                const int cd = quant_exact(x[i], cy.x);
-                                v[i] = __fadd_rn((float)cd, kMagic);
-                                xh[i] = __fmul_rn((float)cd, cy.x);
+                            const float sc = s.cq[sk].s[16 * h + i], yy = s.cq[sk].y[16 * h + i];
+                            const float xi = (i & 1) ? f2hi(X[i / 2]) : f2lo(X[i / 2]);
+                            const float cl = fminf(fmaxf(__fmul_rn(xi, yy), -127.0f), 127.0f);
+                            float vv = __fadd_rn(cl, kMagic);
+                            const float rr = __fsub_rn(vv, kMagic);
+                            float xh = __fmul_rn(rr, sc);
+                            if (fabsf(__fsub_rn(cl, rr)) > kDangerThr || (yy == 0.0f && sc != 0.0f)) {
+                                const int cd = quant_exact(xi, sc);
+                                vv = __fadd_rn((float)cd, kMagic);
+                                xh = __fmul_rn((float)cd, sc);
+                            }
+                            const int j = i / 2;
+                            if (i & 1) {
+                                V[j] = f2pk(f2lo(V[j]), vv);
+                                XH[j] = f2pk(f2lo(XH[j]), xh);
+                            } else {
+                                V[j] = f2pk(vv, f2hi(V[j]));
+                                XH[j] = f2pk(xh, f2hi(XH[j]));
                             }
                         }
                     }
                     // K_hat overwrites x in the input stage (same swizzled positions, read by this
                     // thread only); the codes go to the group's code buffer.  The store warp writes
                     // both out with TMA and then frees the stage (and the code buffer).
-                    if (kb == kb0) KVQ_WAIT_HOT(&s.cstored[cgrp & 1], ((cgrp >> 1) & 1) ^ 1);
+                    KVQ_TR(11, lane == 0 && warp == CONV_W0);
+                    if (!code_buf_ready) {
+                        KVQ_WAIT_HOT(&s.cstored[cgrp & 1], ((cgrp >> 1) & 1) ^ 1);
+                        code_buf_ready = true;
+                    }
                     const uint32_t cds = smem_u32(s.buf + 128 * 1024 + (cgrp & 1) * KTILE);
 #pragma unroll
                     for (int c = 0; c < 4; c++)
-                        sts128(swz(kbase, r, 4 * h + c),
-                               make_float4(xh[4 * c], xh[4 * c + 1], xh[4 * c + 2], xh[4 * c + 3]));
+                        sts128(swz(kbase, r, 4 * h + c), make_float4(f2lo(XH[2 * c]), f2hi(XH[2 * c]),
+                                                                     f2lo(XH[2 * c + 1]), f2hi(XH[2 * c + 1])));
                     uint4 w;
-                    w.x = pack4(v[0], v[1], v[2], v[3]);
-                    w.y = pack4(v[4], v[5], v[6], v[7]);
-                    w.z = pack4(v[8], v[9], v[10], v[11]);
-                    w.w = pack4(v[12], v[13], v[14], v[15]);
+                    w.x = pack4(f2lo(V[0]), f2hi(V[0]), f2lo(V[1]), f2hi(V[1]));
+                    w.y = pack4(f2lo(V[2]), f2hi(V[2]), f2lo(V[3]), f2hi(V[3]));
+                    w.z = pack4(f2lo(V[4]), f2hi(V[4]), f2lo(V[5]), f2hi(V[5]));
+                    w.w = pack4(f2lo(V[6]), f2hi(V[6]), f2lo(V[7]), f2hi(V[7]));
                     sts128u(swz(cds, r, (kb % CODE_KB) * 2 + h), w);
+                    KVQ_TR(12, lane == 0 && warp == CONV_W0);
                     fence_proxy_async();  // generic smem writes -> visible to the TMA (async proxy)
-                    mbar_arrive(&s.staged[sk]);
+                    KVQ_TR(13, lane == 0 && warp == CONV_W0);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&s.staged[sk]);
+                    KVQ_TR(2, lane == 0 && warp == CONV_W0);
                     if (kb == kb1 - 1) cgrp++;
 #pragma unroll
-                    for (int i = 0; i < 16; i++) e[i] = __fsub_rn(x[i], xh[i]);  // exact (fact 4)
+                    for (int j = 0; j < 8; j++) E[j] = f2sub(X[j], XH[j]);  // exact (fact 4)
                 }
                 if (MODE != 1) {
-                    // e^2 summed over the 16 columns in fp32, blocks carried in fp64
-                    float blk = 0.0f;
+                    // e^2 summed over the 16 columns in fp32 (two interleaved partial sums), blocks carried in fp64
+                    uint64_t sq = f2mul(E[0], E[0]);
 #pragma unroll
-                    for (int i = 0; i < 16; i++) {
-                        blk = fmaf(e[i], e[i], blk);
-                        mx = fmaxf(mx, fabsf(e[i]));
-                    }
-                    ss += (double)blk;
+                    for (int j = 1; j < 8; j++) sq = f2fma(E[j], E[j], sq);
+#pragma unroll
+                    for (int j = 0; j < 8; j++) mx = fmaxf(mx, fmaxf(fabsf(f2lo(E[j])), fabsf(f2hi(E[j]))));
+                    ss += (double)__fadd_rn(f2lo(sq), f2hi(sq));
                 }
                 // 3xTF32 split: hi = e with the 13 low mantissa bits cleared (a tf32 value),
                 // lo = e - hi exactly (the tensor core reads lo's top 11 bits: error <= 2^-21 |e|)
                 uint32_t hi[16], lo[16];
 #pragma unroll
-                for (int i = 0; i < 16; i++) {
-                    hi[i] = __float_as_uint(e[i]) & 0xFFFFE000u;
-                    lo[i] = __float_as_uint(__fsub_rn(e[i], __uint_as_float(hi[i])));
+                for (int j = 0; j < 8; j++) {
+                    hi[2 * j] = __float_as_uint(f2lo(E[j])) & 0xFFFFE000u;
+                    hi[2 * j + 1] = __float_as_uint(f2hi(E[j])) & 0xFFFFE000u;
+                    const uint64_t l = f2sub(E[j], f2pk(__uint_as_float(hi[2 * j]), __uint_as_float(hi[2 * j + 1])));
+                    lo[2 * j] = __float_as_uint(f2lo(l));
+                    lo[2 * j + 1] = __float_as_uint(f2hi(l));
                 }
                 const int sa = g % AST;
                 KVQ_WAIT_HOT(&s.empty_a[sa], ((g / AST) & 1) ^ 1);
+                KVQ_TR(3, lane == 0 && warp == CONV_W0);
                 tc_fence_after();
                 tmem_st16(tbase + lane_off + A_COL0 + sa * 64 + 16 * h, hi);
                 tmem_st16(tbase + lane_off + A_COL0 + sa * 64 + 32 + 16 * h, lo);
                 tmem_wait_st();
                 tc_fence_before();
-                mbar_arrive(&s.full_a[sa]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s.full_a[sa]);
+                KVQ_TR(4, lane == 0 && warp == CONV_W0); KVQ_TR(6, lane == 0 && warp == EPI_W0 - 1);
             }
         }
         if (MODE != 1) {
@@ -586,55 +672,113 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
         }
     } else {
-        // ------------------------------------------------------------ epilogue (warps 12..15)
-        setmaxnreg_inc<200>();
+        // ------------------------------------------------------------ epilogue (the last warpgroup)
+        // Chunk sums (fp32 from the tensor core, 128 columns each) are carried across the tile: in fp64
+        // registers with one converter team; with two teams (whose registers leave the epilogue 64) as
+        // error-free (hi, lo) fp32 pairs in the 128 spare TMEM columns ACC_COL0.. .  (Restarting the
+        // accumulator every 128 columns bounds the bias of the tensor core's truncating accumulation.)
+        if constexpr (REG_EPI > REG_LAUNCH)
+            setmaxnreg_inc<REG_EPI>();
+        else if constexpr (REG_EPI < REG_LAUNCH)
+            setmaxnreg_dec<REG_EPI>();
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         double attn = 0.0;
         uint32_t gc = 0;
-        double acc[BN];
+        double acc[NTEAMS == 1 ? BN : 1];
         int piece_grp0 = 0;
         for (UnitWalk w(us); w.ok(); w.next(), gc++) {
             const int tile = w.tile, grp = w.grp;
-            if (grp == 0 || w.i == w.nfull) {  // first unit of this CTA's piece of the tile
-                piece_grp0 = grp;
-#pragma unroll
-                for (int j = 0; j < BN; j++) acc[j] = 0.0;
-            }
+            const bool first = grp == 0 || w.i == w.nfull;  // first unit of this CTA's piece of the tile
+            if (first) piece_grp0 = grp;
             const int ab = gc & 1;
             mbar_wait_sleep(&s.full_acc[ab], (gc >> 1) & 1);
             tc_fence_after();
-            uint32_t v[32];
+            if constexpr (NTEAMS == 1) {
+                if (first) {
 #pragma unroll
-            for (int hh = 0; hh < BN / 32; hh++) {
-                tmem_ld32(tbase + lane_off + ab * BN + 32 * hh, v);
-                tmem_wait_ld();
+                    for (int j = 0; j < BN; j++) acc[j] = 0.0;
+                }
+                uint32_t v[32];
 #pragma unroll
-                for (int j = 0; j < 32; j++) acc[32 * hh + j] += (double)__uint_as_float(v[j]);
+                for (int hh = 0; hh < BN / 32; hh++) {
+                    tmem_ld32(tbase + lane_off + ab * BN + 32 * hh, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 32; j++) acc[32 * hh + j] += (double)__uint_as_float(v[j]);
+                }
+            } else {
+                // running sum (hi, lo) as an unevaluated fp32 pair (Knuth TwoSum per chunk: error-free
+                // addition, so the carry is as accurate as the fp64 one it replaces)
+#pragma unroll 1
+                for (int hh = 0; hh < BN / 8; hh++) {
+                    uint32_t v[8], a[8], b[8];
+                    const uint32_t thi = tbase + lane_off + ACC_COL0 + 8 * hh, tlo = thi + BN;
+                    tmem_ld8(tbase + lane_off + ab * BN + 8 * hh, v);
+                    if (!first) {
+                        tmem_ld8(thi, a);
+                        tmem_ld8(tlo, b);
+                    }
+                    tmem_wait_ld();
+                    if (first) {
+#pragma unroll
+                        for (int j = 0; j < 8; j++) b[j] = 0u;
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; j += 2) {
+                            const uint64_t x = f2pk(__uint_as_float(a[j]), __uint_as_float(a[j + 1]));
+                            const uint64_t y = f2pk(__uint_as_float(v[j]), __uint_as_float(v[j + 1]));
+                            const uint64_t sm = f2add(x, y);
+                            const uint64_t yy = f2sub(sm, x);
+                            const uint64_t er = f2add(f2sub(x, f2sub(sm, yy)), f2sub(y, yy));
+                            const uint64_t lo = f2add(f2pk(__uint_as_float(b[j]), __uint_as_float(b[j + 1])), er);
+                            v[j] = __float_as_uint(f2lo(sm));
+                            v[j + 1] = __float_as_uint(f2hi(sm));
+                            b[j] = __float_as_uint(f2lo(lo));
+                            b[j + 1] = __float_as_uint(f2hi(lo));
+                        }
+                    }
+                    tmem_st8(thi, v);
+                    tmem_st8(tlo, b);
+                }
+                tmem_wait_st();
             }
             tc_fence_before();
             mbar_arrive(&s.empty_acc[ab]);
             if (w.i != w.n - 1 && grp != ngrp - 1) continue;  // piece not finished
-            if (piece_grp0 == 0 && grp == ngrp - 1) {
-                // the whole tile row-block is this CTA's: Delta is complete
-                const int64_t row = (int64_t)tile * BM + r;
-                if (row < T) {
+            const bool whole = piece_grp0 == 0 && grp == ngrp - 1;  // the whole tile row-block is this CTA's
+            const int64_t row = (int64_t)tile * BM + r;
+            // a piece of a split tile: slot 0 if it starts inside the tile, else slot 1
+            double *slot = p.split + ((int64_t)blockIdx.x * 2 + (piece_grp0 != 0 ? 0 : 1)) * (BN * BM);
+#pragma unroll 1
+            for (int hh = 0; hh < (NTEAMS == 1 ? 1 : BN / 8); hh++) {
+                constexpr int NJ = NTEAMS == 1 ? BN : 8;
+                uint32_t a[8], b[8];
+                if constexpr (NTEAMS > 1) {
+                    tmem_ld8(tbase + lane_off + ACC_COL0 + 8 * hh, a);
+                    tmem_ld8(tbase + lane_off + ACC_COL0 + BN + 8 * hh, b);
+                    tmem_wait_ld();
+                }
 #pragma unroll
-                    for (int j = 0; j < BN; j++) {
-                        if (j < nq) {
+                for (int jj = 0; jj < NJ; jj++) {
+                    const int j = (NTEAMS == 1 ? 0 : 8 * hh) + jj;
+                    double dv;
+                    if constexpr (NTEAMS == 1)
+                        dv = acc[jj];
+                    else
+                        dv = (double)__uint_as_float(a[jj]) + (double)__uint_as_float(b[jj]);
+                    if (whole) {
+                        if (row < T && j < nq) {
                             if (MODE != 1)
-                                attn += fabs(acc[j]);
+                                attn += fabs(dv);
                             else
-                                p.S[(int64_t)j * T + row] = (float)acc[j];
+                                p.S[(int64_t)j * T + row] = (float)dv;
                         }
+                    } else if (MODE != 1) {
+                        slot[j * BM + r] = dv;
                     }
                 }
-            } else if (MODE != 1) {
-                // a piece of a split tile: slot 0 if it starts inside the tile, else slot 1
-                double *slot = p.split + ((int64_t)blockIdx.x * 2 + (piece_grp0 != 0 ? 0 : 1)) * (BN * BM);
-#pragma unroll
-                for (int j = 0; j < BN; j++) slot[j * BM + r] = acc[j];
             }
         }
         if (MODE != 1) {
@@ -646,7 +790,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncthreads();
     if (MODE != 1 && threadIdx.x == 0) {
         Partial pt{0.0, 0.0, 0.0, 0.0};
-        for (int i = 0; i < 8; i++) {  // fixed order: deterministic
+        for (int i = 0; i < NTEAMS * 8; i++) {  // fixed order: deterministic
             pt.sum_sq += s.red[0][i];
             pt.max_abs = fmax(pt.max_abs, s.red[2][i]);
         }
@@ -805,3 +949,9 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
 }
 
 }  // namespace kvq
+
+#ifdef KVQ_TRACE
+extern "C" int kvq_debug_trace_read(void *host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, kvq::tc::g_kvq_trace, bytes < sizeof(kvq::tc::g_kvq_trace) ? bytes : sizeof(kvq::tc::g_kvq_trace));
+}
+#endif
