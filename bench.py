@@ -38,7 +38,7 @@ CONFIGS = {  # BASELINE.json configs
 METRIC = "quantize+dequantize elements/s and achieved HBM GB/s vs B200 peak at 1/2/4/8 GPUs"
 # Algorithmic bytes per element of each pass: what the method itself must move.
 SPIN_CYCLES = 100_000  # ~50 us device spin queued ahead of each timed step (keeps launch latency out)
-BYTES = {"scales": 4, "quantize": 5, "dequantize": 5, "metrics": 8, "roundtrip": 9, "quantize_dequantize_e4m3": 9,
+BYTES = {"step": 13, "scales": 4, "quantize": 5, "dequantize": 5, "metrics": 8, "roundtrip": 9, "quantize_dequantize_e4m3": 9,
          "quantize_dequantize_int4": 8.5, "quantize_dequantize_int2": 8.25}
 
 
@@ -258,7 +258,9 @@ def launches_per_step(args, comm, comm_kind, rows, D):
     peer = comm is not None and comm_kind is not None and comm_kind.startswith("peer")
     scales = 1 if peer else 2
     tail = 0 if comm is None else (2 if peer else 1)
-    if args.format == "int8" and args.pipeline == "fused":
+    if args.format == "int8" and args.pipeline == "step" and comm is None and D <= 256 and rows * D <= (1 << 20):
+        return 1  # csrc/step_small.cu: the whole step in one cooperative launch
+    if args.format == "int8" and args.pipeline in ("fused", "step"):
         return scales + 3 + combine + tail
     metrics = 3 + combine + tail
     if args.format == "int8":
@@ -372,7 +374,21 @@ def run_kvq(args, cfg, rank, world, local_rank):
         if ev is not None:
             ev[3].record(stream)
 
-    if args.format == "e4m3":
+    wstep = None
+    if args.pipeline == "step":
+        wstep = torch.empty(kvq.kvq_step_workspace_size(rows, D, nq), dtype=torch.uint8, device=dev)
+
+    def step_one(ev=None):
+        """kvq_step: the whole path in ONE ABI call (one cooperative launch for small problems)."""
+        if ev is not None:
+            ev[0].record(stream)
+        kvq.kvq_step(K, Q, scales, Kq, Kh, out_dev=mout, workspace=wstep, comm=comm, stream=stream)
+        if ev is not None:
+            ev[1].record(stream)
+
+    if args.pipeline == "step":
+        step, pass_names = step_one, ["step"]
+    elif args.format == "e4m3":
         step, pass_names = step_e4m3, ["scales", "quantize_dequantize_e4m3", "metrics"]
     elif bits:
         step, pass_names = step_lowbit, ["scales", f"quantize_dequantize_{args.format}", "metrics"]
@@ -537,7 +553,8 @@ def run_kvq(args, cfg, rank, world, local_rank):
         "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (splitmix64 lattice uniform [-1,1), SURVEY §8(d))",
         "config": {"workload": f"{cfg['name']}: {cfg['desc']}", "T": T, "D": D, "nq": nq,
-                   "step": ("kvq_compute_scales_fmt(E4M3) -> kvq_quantize_e4m3(+K_hat) -> kvq_error_metrics_async"
+                   "step": "kvq_step (a1, a7, a2, a3, a4, a5, a6 in one ABI call)" if args.pipeline == "step" else
+                           ("kvq_compute_scales_fmt(E4M3) -> kvq_quantize_e4m3(+K_hat) -> kvq_error_metrics_async"
                             if args.format == "e4m3" else
                             f"kvq_compute_scales_fmt({args.format.upper()}) -> kvq_quantize_packed(bits={bits}, +K_hat)"
                             " -> kvq_error_metrics_async" if bits else
@@ -586,7 +603,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="kvq", choices=["kvq", "reference"])
-    ap.add_argument("--pipeline", default="fused", choices=["fused", "separate"])
+    ap.add_argument("--pipeline", default="fused", choices=["fused", "separate", "step"],
+                    help="fused = kvq_compute_scales + kvq_roundtrip (per-pass events); separate = the four "
+                         "calls; step = kvq_step (one call; one cooperative launch for small problems)")
     ap.add_argument("--format", default="int8", choices=["int8", "e4m3", "int4", "int2"],
                     help="int8 = the paper's method (headline); e4m3 = the FP8 variant (NEXT-1); "
                          "int4 / int2 = the packed low-bit variants (NEXT-3)")

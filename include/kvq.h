@@ -260,6 +260,26 @@ kvq_status kvq_roundtrip(const float *K, const float *scales, int64_t T, int64_t
                          float *K_hat, const float *Q, int64_t nq, void *workspace,
                          size_t workspace_bytes, kvq_comm_t comm, kvq_metrics *out_dev, void *stream);
 
+/* The whole hot path on device buffers in one call (a1 column abs-max over K, a7
+ * the all-reduce MAX of the column maxima over the token shards when comm != NULL,
+ * a2 scales, then a3-a6 as kvq_roundtrip): kvq_compute_scales + kvq_roundtrip.
+ * Alg. 1, Eq. 7/8, fidelity checks P:20-24.
+ * K: [T][D] (this rank's token shard when comm != NULL); Q: [nq][D] or NULL;
+ * outputs scales [D] (global, identical on every rank), Kq [T][D], K_hat [T][D] and
+ * out_dev (DEVICE kvq_metrics), all caller-owned, written asynchronously on `stream`.
+ * Small single-GPU problems (comm == NULL, D <= 256, nq <= 64, T*D <= 2^20, e.g.
+ * BASELINE C1) run as ONE cooperative launch (grid-wide barriers between the
+ * paper's steps; a6 with exact fp64 products and sums on the CUDA cores); everything else
+ * runs the streaming column max and the single-pass tensor-core roundtrip.  Both
+ * give bit-identical scales, codes and K_hat; metrics within rounding of fp64 sums.
+ * workspace: kvq_step_workspace_size(T, D, nq) bytes, any alignment; not shared by
+ * concurrent calls.  Errors as kvq_roundtrip (KVQ_ERR_INVALID_VALUE on NULL/alias/
+ * small workspace before anything is enqueued). */
+size_t kvq_step_workspace_size(int64_t T, int64_t D, int64_t nq);
+kvq_status kvq_step(const float *K, int64_t T, int64_t D, const float *Q, int64_t nq, float *scales,
+                    int8_t *Kq, float *K_hat, void *workspace, size_t workspace_bytes, kvq_comm_t comm,
+                    kvq_metrics *out_dev, void *stream);
+
 /* Raw attention scores for parity checks of a6 (reading Q10):
  *   K_hat == NULL:  S[i][t] = sum_d Q[i][d] * K[t][d]
  *   K_hat != NULL:  S[i][t] = sum_d Q[i][d] * (K[t][d] - K_hat[t][d])   (= S - S')

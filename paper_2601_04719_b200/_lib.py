@@ -58,6 +58,8 @@ SIGNATURES = {
                                  ctypes.POINTER(kvq_metrics), _vp]),
     "kvq_roundtrip_workspace_size": (_sz, [_i64, _i64, _i64]),
     "kvq_roundtrip": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _vp, _sz, _vp, _vp, _vp]),
+    "kvq_step_workspace_size": (_sz, [_i64, _i64, _i64]),
+    "kvq_step": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp, _vp, _vp]),
     "kvq_attention_scores_workspace_size": (_sz, [_i64, _i64]),
     "kvq_attention_scores": (_int, [_vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     "kvq_scores_from_codes_workspace_size": (_sz, [_i64, _i64]),

@@ -397,6 +397,36 @@ extern "C" kvq_status kvq_roundtrip(const float *K, const float *scales, int64_t
     return launch_metrics_finalize(tot, out_dev, s);
 }
 
+extern "C" size_t kvq_step_workspace_size(int64_t T, int64_t D, int64_t nq) {
+    if (bad_dims(T, D) || nq < 0) return 0;
+    return std::max(kvq_roundtrip_workspace_size(T, D, nq), step_small_workspace_size(T, D));
+}
+
+extern "C" kvq_status kvq_step(const float *K, int64_t T, int64_t D, const float *Q, int64_t nq, float *scales,
+                               int8_t *Kq, float *K_hat, void *workspace, size_t workspace_bytes, kvq_comm_t comm,
+                               kvq_metrics *out_dev, void *stream) {
+    KVQ_REQUIRE(K && scales && Kq && K_hat && workspace && out_dev, "kvq_step: NULL pointer");
+    KVQ_REQUIRE(!bad_dims(T, D), "kvq_step: need T >= 1, D >= 1, T*D <= 2^62");
+    KVQ_REQUIRE(nq >= 0 && (nq == 0 || Q), "kvq_step: need nq >= 0 and Q when nq > 0");
+    KVQ_REQUIRE(nq <= (int64_t(1) << 62) / D && nq <= (int64_t(1) << 62) / T, "kvq_step: nq too large");
+    const size_t n = (size_t)(T * D);
+    KVQ_REQUIRE(!overlap(K, n * 4, Kq, n) && !overlap(K_hat, n * 4, K, n * 4) && !overlap(K_hat, n * 4, Kq, n) &&
+                    !overlap(scales, (size_t)D * 4, K, n * 4) && !overlap(scales, (size_t)D * 4, Kq, n) &&
+                    !overlap(scales, (size_t)D * 4, K_hat, n * 4),
+                "kvq_step: outputs alias inputs");
+    KVQ_REQUIRE(!overlap(workspace, workspace_bytes, Kq, n) && !overlap(workspace, workspace_bytes, K_hat, n * 4) &&
+                    !overlap(workspace, workspace_bytes, scales, (size_t)D * 4),
+                "kvq_step: workspace aliases an output");
+    KVQ_REQUIRE(workspace_bytes >= kvq_step_workspace_size(T, D, nq), "kvq_step: workspace too small");
+    KVQ_TRY(device_ok());
+    cudaStream_t s = (cudaStream_t)stream;
+    if (step_small_eligible(T, D, nq, comm))
+        return launch_step_small(K, T, D, nq ? Q : nullptr, nq, scales, Kq, K_hat, workspace, workspace_bytes,
+                                 out_dev, s);
+    KVQ_TRY(kvq_compute_scales(K, T, D, scales, comm, stream));
+    return kvq_roundtrip(K, scales, T, D, Kq, K_hat, Q, nq, workspace, workspace_bytes, comm, out_dev, stream);
+}
+
 extern "C" size_t kvq_attention_scores_workspace_size(int64_t D, int64_t nq) {
     if (D < 1 || nq < 1) return 0;
     return attention_scores_workspace_size(D, nq);

@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         double attn = 0.0;
         uint32_t gc = 0;
-        double acc[NTEAMS == 1 ? BN : 1];
+        [[maybe_unused]] double acc[NTEAMS == 1 ? BN : 1];
         int piece_grp0 = 0;
         for (UnitWalk w(us); w.ok(); w.next(), gc++) {
             const int tile = w.tile, grp = w.grp;

@@ -104,6 +104,13 @@ size_t attention_scores_workspace_size(int64_t D, int64_t nq);
 kvq_status launch_attention_scores(const float *Q, int64_t nq, const float *K, const float *K_hat, int64_t T,
                                    int64_t D, float *S, void *ws, size_t ws_bytes, cudaStream_t s);
 
+// ---- the whole step in one cooperative launch for small problems (step_small.cu, NEXT-4)
+bool step_small_eligible(int64_t T, int64_t D, int64_t nq, kvq_comm_t comm);
+size_t step_small_workspace_size(int64_t T, int64_t D);
+kvq_status launch_step_small(const float *K, int64_t T, int64_t D, const float *Q, int64_t nq, float *scales,
+                             int8_t *Kq, float *K_hat, void *ws, size_t ws_bytes, kvq_metrics *out_dev,
+                             cudaStream_t s);
+
 // ---- scores from codes (scores_codes.cu, NEXT-2)
 size_t scores_codes_workspace_size(int64_t D);
 kvq_status launch_scores_codes(const float *Q, int64_t nq, const int8_t *Kq, const float *scales, int64_t T,

@@ -381,13 +381,13 @@ __device__ __forceinline__ uint64_t f2pk(float a, float b) {
     return r;
 }
 __device__ __forceinline__ float f2lo(uint64_t r) {
-    float a, b;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+    float a;
+    asm("{\n\t.reg .b32 t;\n\tmov.b64 {%0, t}, %1;\n\t}" : "=f"(a) : "l"(r));
     return a;
 }
 __device__ __forceinline__ float f2hi(uint64_t r) {
-    float a, b;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+    float b;
+    asm("{\n\t.reg .b32 t;\n\tmov.b64 {t, %0}, %1;\n\t}" : "=f"(b) : "l"(r));
     return b;
 }
 __device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {

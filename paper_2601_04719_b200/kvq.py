@@ -57,6 +57,31 @@ def _vec(t: torch.Tensor, n: int, name: str):
         raise ValueError(f"{name}: expected contiguous CUDA float32[{n}]")
 
 
+def _out(t: torch.Tensor, shape, dtype, name: str, cuda: bool = True):
+    """Caller-supplied output: exact shape and dtype, contiguous, on the right side (the library writes
+    shape-many elements through the raw pointer; a smaller or host buffer would be overrun or faulted)."""
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    if cuda and not t.is_cuda:
+        raise ValueError(f"{name}: must be a CUDA tensor")
+    if not cuda and t.is_cuda:
+        raise ValueError(f"{name}: must be a host tensor")
+    return t
+
+
+def _buf(t: torch.Tensor, nbytes: int, name: str, cuda: bool = True):
+    """Caller-supplied byte buffer (workspace, metrics output): at least nbytes, contiguous, right side."""
+    if not t.is_contiguous() or t.numel() * t.element_size() < nbytes:
+        raise ValueError(f"{name}: need a contiguous buffer of >= {nbytes} bytes")
+    if cuda != t.is_cuda:
+        raise ValueError(f"{name}: must be a {'CUDA' if cuda else 'host'} tensor")
+    return t
+
+
 def _comm_handle(comm):
     return None if comm is None else comm.handle
 
@@ -426,6 +451,38 @@ def kvq_roundtrip(K: torch.Tensor, scales: torch.Tensor, Q: Optional[torch.Tenso
                                workspace.numel(), _comm_handle(comm), _ptr(out_dev), _stream(stream)),
           "kvq_roundtrip")
     return Kq, K_hat, out_dev
+
+
+def kvq_step_workspace_size(T: int, D: int, nq: int) -> int:
+    return int(load().kvq_step_workspace_size(T, D, nq))
+
+
+def kvq_step(K: torch.Tensor, Q: Optional[torch.Tensor] = None, scales: Optional[torch.Tensor] = None,
+             Kq: Optional[torch.Tensor] = None, K_hat: Optional[torch.Tensor] = None,
+             out_dev: Optional[torch.Tensor] = None, workspace=None, comm: Optional[Comm] = None, stream=None):
+    """The whole hot path in one call (a1 + a7 + a2 scales, then a3-a6).  Returns (scales, Kq, K_hat,
+    out_dev) with out_dev a device kvq_metrics (metrics_from_device)."""
+    T, D = _mat(K, torch.float32, "K")
+    nq = 0
+    if Q is not None:
+        nq, Dq = _mat(Q, torch.float32, "Q")
+        if Dq != D:
+            raise ValueError("Q: expected D columns")
+    dev = K.device
+    scales = _out(scales if scales is not None else torch.empty(D, dtype=torch.float32, device=dev), (D,),
+                  torch.float32, "scales")
+    Kq = _out(Kq if Kq is not None else torch.empty((T, D), dtype=torch.int8, device=dev), (T, D), torch.int8, "Kq")
+    K_hat = _out(K_hat if K_hat is not None else torch.empty((T, D), dtype=torch.float32, device=dev), (T, D),
+                 torch.float32, "K_hat")
+    need = kvq_step_workspace_size(T, D, nq)
+    workspace = _buf(workspace if workspace is not None else torch.empty(need, dtype=torch.uint8, device=dev), need,
+                     "workspace")
+    out_dev = _buf(out_dev if out_dev is not None else torch.empty(METRICS_BYTES, dtype=torch.uint8, device=dev),
+                   METRICS_BYTES, "out_dev")
+    check(load().kvq_step(_ptr(K), T, D, _ptr(Q), nq, _ptr(scales), _ptr(Kq), _ptr(K_hat), _ptr(workspace),
+                          workspace.numel() * workspace.element_size(), _comm_handle(comm), _ptr(out_dev),
+                          _stream(stream)), "kvq_step")
+    return scales, Kq, K_hat, out_dev
 
 
 def kvq_attention_scores(Q: torch.Tensor, K: torch.Tensor, K_hat: Optional[torch.Tensor] = None,
