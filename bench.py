@@ -255,7 +255,7 @@ def launches_per_step(args, comm, comm_kind, rows, D):
     r0 = ntiles % nsm
     cut = ntiles >= nsm and r0 > 0 and any(ngrp % c == 0 and r0 * c <= nsm for c in range(2, ngrp + 1))
     combine = 1 if cut else 0  # left-over tiles cut into pieces (attn_tc.cu launch_attn_tc)
-    peer = comm is not None and comm_kind is not None and comm_kind.startswith("peer")
+    peer = comm is not None and comm_kind is not None and comm_kind.startswith(("peer", "nvls"))
     scales = 1 if peer else 2
     tail = 0 if comm is None else (2 if peer else 1)
     if args.format == "int8" and args.pipeline == "step" and comm is None and D <= 256 and rows * D <= (1 << 20):
@@ -273,7 +273,8 @@ def run_kvq(args, cfg, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2601_04719_b200 import kvq
-    from paper_2601_04719_b200.dist import make_comm, make_peer, max_over_ranks, max_over_ranks_vec, shard_rows
+    from paper_2601_04719_b200.dist import (enable_nvls, make_comm, make_peer, max_over_ranks, max_over_ranks_vec,
+                                            shard_rows)
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -288,11 +289,16 @@ def run_kvq(args, cfg, rank, world, local_rank):
     # kernels.  Without torchrun there is nothing to exchange.
     comm, peer, comm_kind = None, None, None
     if dist.is_available() and dist.is_initialized():
-        if args.comm == "peer":
+        if args.comm in ("peer", "nvls"):
             try:
                 peer = make_peer(rank, world, cfg["D"])
                 comm = kvq.Comm.from_peer(peer)
                 comm_kind = "peer (CUDA-IPC peer memory, libkvq kvq_comm_from_peer; no NCCL)"
+                if args.comm == "nvls":
+                    if enable_nvls(peer, rank, world):
+                        comm_kind = "nvls (a7 max by multimem.ld_reduce in the NVSwitch; metrics over peer memory)"
+                    else:
+                        comm_kind = f"peer (NVLS unavailable: {getattr(peer, 'nvls_reason', '')[:80]})"
             except Exception as e:  # e.g. no peer access between the GPUs: NCCL instead
                 comm_kind = f"nccl (peer setup failed: {str(e)[:80]})"
         if comm is None:
@@ -609,9 +615,10 @@ def main():
     ap.add_argument("--format", default="int8", choices=["int8", "e4m3", "int4", "int2"],
                     help="int8 = the paper's method (headline); e4m3 = the FP8 variant (NEXT-1); "
                          "int4 / int2 = the packed low-bit variants (NEXT-3)")
-    ap.add_argument("--comm", default="peer", choices=["peer", "nccl"],
+    ap.add_argument("--comm", default="peer", choices=["peer", "nvls", "nccl"],
                     help="collectives under torchrun: peer = CUDA-IPC peer memory (a7 fused into the column-max "
-                         "kernel, metric partials by one exchange kernel; no NCCL), nccl = NCCL all-reduces")
+                         "kernel, metric partials by one exchange kernel; no NCCL), nvls = the same with the a7 max "
+                         "read through NVLS multicast when every GPU can map it, nccl = NCCL all-reduces")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=12)

@@ -218,6 +218,27 @@ kvq_status kvq_comm_from_peer(kvq_comm_t *out, kvq_peer_t p);
 kvq_status kvq_peer_init(kvq_peer_t *out, int nranks, int rank, int64_t D, void *handle_out);
 kvq_status kvq_peer_open(kvq_peer_t p, const void *handles);
 kvq_status kvq_peer_destroy(kvq_peer_t p);
+
+/* NVLS (NVLink SHARP) for the peer's a7 exchange (multi-GPU is the
+ * paper's future work).  With NVLS active, the last CTA of the fused column-max kernel
+ * stores the rank's D column maxima into its OWN copy of a multicast-bound buffer and, after
+ * the epoch flags, reads m_d with one multimem.ld_reduce.max.u32 per column: the NVSwitch reads
+ * every rank's copy and returns the max (order-free, so scales stay bit-identical).  Setup is
+ * collective and staged so that no rank blocks on a rank that failed:
+ *   rank 0:     kvq_peer_nvls_create(p, blob)  multicast object for nranks devices; [host] blob
+ *               of kvq_peer_nvls_handle_bytes() bytes to broadcast (a fabric handle, or the tag
+ *               of a unix socket on which rank 0's process hands out a POSIX fd for it)
+ *   every rank: kvq_peer_nvls_join(p, blob)    import + cuMulticastAddDevice
+ *   (all joined) kvq_peer_nvls_map(p)          own memory, bind, multicast + unicast mappings
+ *   (all mapped) kvq_peer_nvls_enable(p, 1)    or (p, 0) on every rank to release and keep P2P
+ * Errors: KVQ_ERR_UNSUPPORTED when the device, driver or handle exchange cannot do multicast
+ * (resources released; the P2P exchange keeps working).  p must be open (kvq_peer_open). */
+size_t kvq_peer_nvls_handle_bytes(void);
+kvq_status kvq_peer_nvls_create(kvq_peer_t p, void *blob_out);
+kvq_status kvq_peer_nvls_join(kvq_peer_t p, const void *blob);
+kvq_status kvq_peer_nvls_map(kvq_peer_t p);
+kvq_status kvq_peer_nvls_enable(kvq_peer_t p, int on);
+int kvq_peer_nvls_active(kvq_peer_t p);
 kvq_status kvq_compute_scales_peer(const float *K, int64_t T, int64_t D, float *scales, kvq_peer_t p, void *stream);
 
 /* a5+a6: the paper's fidelity checks.

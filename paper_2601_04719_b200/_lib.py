@@ -74,6 +74,12 @@ SIGNATURES = {
     "kvq_peer_init": (_int, [ctypes.POINTER(_vp), _int, _int, _i64, _vp]),
     "kvq_peer_open": (_int, [_vp, _vp]),
     "kvq_peer_destroy": (_int, [_vp]),
+    "kvq_peer_nvls_handle_bytes": (_sz, []),
+    "kvq_peer_nvls_create": (_int, [_vp, _vp]),
+    "kvq_peer_nvls_join": (_int, [_vp, _vp]),
+    "kvq_peer_nvls_map": (_int, [_vp]),
+    "kvq_peer_nvls_enable": (_int, [_vp, _int]),
+    "kvq_peer_nvls_active": (_int, [_vp]),
     "kvq_compute_scales_peer": (_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
 }
 

@@ -24,11 +24,19 @@
 // order.  Every rank must call kvq_compute_scales_peer the same number of times in
 // the same order (like NCCL), and the ranks' kernels must be able to run
 // concurrently (one GPU per rank, or time-sliced processes on one GPU in tests).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <sys/socket.h>
+#include <sys/un.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
+#include <mutex>
+#include <random>
 #include <string>
+#include <thread>
 
 #include "device_common.cuh"
 #include "kvq_internal.h"
@@ -37,6 +45,8 @@ constexpr int kPeerMax = 16;
 
 struct PeerArgs {
     uint32_t *bufs[kPeerMax];  // every rank's exchange buffer (bufs[rank] = this rank's own)
+    uint32_t *mc;              // NVLS: multicast mapping of the column slots (nullptr: P2P slot stores)
+    uint32_t *uc;              // NVLS: this rank's own physical copy of them (unicast mapping)
     unsigned *ticket;          // grid-wide ticket (this rank's buffer)
     int nranks, rank;
     int64_t D, slot_stride;    // u32 per slot (D rounded up to 64)
@@ -59,6 +69,16 @@ struct kvq_peer_s {
     uint32_t *bufs[kPeerMax];
     uint64_t epoch;
     bool open;
+    // NVLS (NVLink SHARP multicast): the a7 column maxima reduced inside the NVSwitch
+    struct {
+        bool joined = false, mapped = false, active = false;
+        unsigned long long mc = 0, mem = 0;  // CUmemGenericAllocationHandle of the multicast object / own memory
+        unsigned long long mc_va = 0, uc_va = 0;
+        size_t bytes = 0;
+        int device = -1;
+        std::thread server;  // POSIX-fd export: hands the fd to the other ranks over a unix socket
+        int listen_fd = -1, export_fd = -1;
+    } nv;
 };
 
 namespace kvq {
@@ -198,9 +218,24 @@ __global__ void __launch_bounds__(kThreads, 6) colmax_peer_kernel(const float4 *
     __threadfence();  // every CTA's atomics on `bits` are visible
     const int64_t D = pa.D;
     const int par = (int)(pa.epoch & 1);
+    const int64_t D4 = D / 4;
+    if (pa.mc) {
+        // NVLS: every rank stores its D-vector into its OWN copy of the parity's slot; after the flags, one
+        // multimem.ld_reduce.max per column makes the NVSwitch read all ranks' copies and return their max
+        uint4 *mine = reinterpret_cast<uint4 *>(pa.uc + (int64_t)par * pa.slot_stride);
+        for (int64_t i = threadIdx.x; i < D4; i += kThreads) mine[i] = __ldcg(reinterpret_cast<const uint4 *>(bits) + i);
+        if (threadIdx.x == 0) *pa.ticket = 0u;
+        peer_signal_wait(pa);
+        const uint32_t *mc = pa.mc + (int64_t)par * pa.slot_stride;
+        for (int64_t d = threadIdx.x; d < D; d += kThreads) {
+            uint32_t m;
+            asm volatile("multimem.ld_reduce.relaxed.sys.global.max.u32 %0, [%1];" : "=r"(m) : "l"(mc + d) : "memory");
+            reinterpret_cast<float *>(bits)[d] = __fdiv_rn(__uint_as_float(m), pa.divisor);  // Eq. 5/6, reading Q3
+        }
+        return;
+    }
     const int64_t my_slot = kHdrU32 + ((int64_t)par * pa.nranks + pa.rank) * pa.slot_stride;
     // 16-byte accesses (D % 4 == 0; slots are 256-byte aligned), independent iterations
-    const int64_t D4 = D / 4;
     for (int64_t i = threadIdx.x; i < D4; i += kThreads) {
         const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(bits) + i);
         for (int r = 0; r < pa.nranks; r++)
@@ -304,9 +339,12 @@ extern "C" kvq_status kvq_peer_open(kvq_peer_t p, const void *handles) {
     return KVQ_OK;
 }
 
+static void nvls_release(kvq_peer_t p);
+
 extern "C" kvq_status kvq_peer_destroy(kvq_peer_t p) {
     if (!p) return KVQ_OK;
     cudaDeviceSynchronize();
+    nvls_release(p);
     for (int r = 0; r < p->nranks; r++)
         if (p->mapped[r]) cudaIpcCloseMemHandle(p->mapped[r]);
     cudaFree(p->local);
@@ -317,6 +355,10 @@ extern "C" kvq_status kvq_peer_destroy(kvq_peer_t p) {
 
 static PeerArgs peer_args(kvq_peer_t p, float divisor) {
     PeerArgs pa{};
+    if (p->nv.active) {
+        pa.mc = reinterpret_cast<uint32_t *>(p->nv.mc_va);
+        pa.uc = reinterpret_cast<uint32_t *>(p->nv.uc_va);
+    }
     for (int r = 0; r < p->nranks; r++) pa.bufs[r] = p->bufs[r];
     pa.ticket = p->local + kFlagsU32;
     pa.nranks = p->nranks;
@@ -395,3 +437,309 @@ extern "C" kvq_status kvq_compute_scales_peer(const float *K, int64_t T, int64_t
     KVQ_TRY(device_ok());
     return peer_compute_scales(K, T, D, scales, 127.0f, p, (cudaStream_t)stream);
 }
+
+// ============================================================================ NVLS (multicast) setup
+// Driver entry points (cuMulticast*, cuMem*) resolved through the runtime: no -lcuda link.
+namespace {
+struct Drv {
+    decltype(&cuDeviceGetAttribute) devAttr = nullptr;
+    decltype(&cuDeviceGet) devGet = nullptr;
+    decltype(&cuMulticastCreate) mcCreate = nullptr;
+    decltype(&cuMulticastAddDevice) mcAdd = nullptr;
+    decltype(&cuMulticastGetGranularity) mcGran = nullptr;
+    decltype(&cuMulticastBindMem) mcBind = nullptr;
+    decltype(&cuMulticastUnbind) mcUnbind = nullptr;
+    decltype(&cuMemCreate) memCreate = nullptr;
+    decltype(&cuMemGetAllocationGranularity) memGran = nullptr;
+    decltype(&cuMemAddressReserve) vaReserve = nullptr;
+    decltype(&cuMemAddressFree) vaFree = nullptr;
+    decltype(&cuMemMap) map = nullptr;
+    decltype(&cuMemUnmap) unmap = nullptr;
+    decltype(&cuMemSetAccess) setAccess = nullptr;
+    decltype(&cuMemRelease) release = nullptr;
+    decltype(&cuMemExportToShareableHandle) exportH = nullptr;
+    decltype(&cuMemImportFromShareableHandle) importH = nullptr;
+    bool ok = false;
+};
+template <typename F>
+bool sym(const char *name, F &f) {
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &ptr, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    f = reinterpret_cast<F>(ptr);
+    return true;
+}
+const Drv &drv() {
+    static Drv d;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        d.ok = sym("cuDeviceGetAttribute", d.devAttr) && sym("cuDeviceGet", d.devGet) &&
+               sym("cuMulticastCreate", d.mcCreate) && sym("cuMulticastAddDevice", d.mcAdd) &&
+               sym("cuMulticastGetGranularity", d.mcGran) && sym("cuMulticastBindMem", d.mcBind) &&
+               sym("cuMulticastUnbind", d.mcUnbind) && sym("cuMemCreate", d.memCreate) &&
+               sym("cuMemGetAllocationGranularity", d.memGran) && sym("cuMemAddressReserve", d.vaReserve) &&
+               sym("cuMemAddressFree", d.vaFree) && sym("cuMemMap", d.map) && sym("cuMemUnmap", d.unmap) &&
+               sym("cuMemSetAccess", d.setAccess) && sym("cuMemRelease", d.release) &&
+               sym("cuMemExportToShareableHandle", d.exportH) &&
+               sym("cuMemImportFromShareableHandle", d.importH);
+    });
+    return d;
+}
+
+// The 128-byte handle blob rank 0 broadcasts: the multicast object as a fabric handle, or (kind 2) the tag
+// of the abstract unix socket on which rank 0's process hands out a POSIX file descriptor for it.
+struct NvlsBlob {
+    uint32_t magic, kind;
+    uint64_t size, tag;
+    uint32_t nranks, pad;
+    unsigned char fabric[64];
+    unsigned char rest[128 - 96];
+};
+static_assert(sizeof(NvlsBlob) == 128, "blob");
+constexpr uint32_t kNvlsMagic = 0x4b56514eu;  // "KVQN"
+
+std::string sock_name(uint64_t tag) { return "kvq-nvls-" + std::to_string(tag); }
+int make_listen(uint64_t tag) {
+    int fd = socket(AF_UNIX, SOCK_STREAM, 0);
+    if (fd < 0) return -1;
+    sockaddr_un a{};
+    a.sun_family = AF_UNIX;
+    const std::string n = sock_name(tag);
+    std::memcpy(a.sun_path + 1, n.data(), n.size());  // abstract namespace (leading NUL)
+    const socklen_t len = (socklen_t)(offsetof(sockaddr_un, sun_path) + 1 + n.size());
+    if (bind(fd, reinterpret_cast<sockaddr *>(&a), len) != 0 || listen(fd, kPeerMax) != 0) {
+        close(fd);
+        return -1;
+    }
+    return fd;
+}
+bool send_fd(int sock, int fd) {
+    char dummy = 'k';
+    iovec iov{&dummy, 1};
+    char ctrl[CMSG_SPACE(sizeof(int))] = {};
+    msghdr m{};
+    m.msg_iov = &iov;
+    m.msg_iovlen = 1;
+    m.msg_control = ctrl;
+    m.msg_controllen = sizeof(ctrl);
+    cmsghdr *c = CMSG_FIRSTHDR(&m);
+    c->cmsg_level = SOL_SOCKET;
+    c->cmsg_type = SCM_RIGHTS;
+    c->cmsg_len = CMSG_LEN(sizeof(int));
+    std::memcpy(CMSG_DATA(c), &fd, sizeof(int));
+    return sendmsg(sock, &m, 0) == 1;
+}
+int recv_fd(uint64_t tag) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {  // rank 0 is already listening when the blob is broadcast; retry briefly anyway
+        int s = socket(AF_UNIX, SOCK_STREAM, 0);
+        if (s < 0) return -1;
+        sockaddr_un a{};
+        a.sun_family = AF_UNIX;
+        const std::string n = sock_name(tag);
+        std::memcpy(a.sun_path + 1, n.data(), n.size());
+        const socklen_t len = (socklen_t)(offsetof(sockaddr_un, sun_path) + 1 + n.size());
+        if (connect(s, reinterpret_cast<sockaddr *>(&a), len) == 0) {
+            char dummy;
+            iovec iov{&dummy, 1};
+            char ctrl[CMSG_SPACE(sizeof(int))] = {};
+            msghdr m{};
+            m.msg_iov = &iov;
+            m.msg_iovlen = 1;
+            m.msg_control = ctrl;
+            m.msg_controllen = sizeof(ctrl);
+            int fd = -1;
+            if (recvmsg(s, &m, 0) == 1) {
+                cmsghdr *c = CMSG_FIRSTHDR(&m);
+                if (c && c->cmsg_type == SCM_RIGHTS) std::memcpy(&fd, CMSG_DATA(c), sizeof(int));
+            }
+            close(s);
+            return fd;
+        }
+        close(s);
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20)) return -1;
+        std::this_thread::sleep_for(std::chrono::milliseconds(20));
+    }
+}
+}  // namespace
+
+static void nvls_release(kvq_peer_t p) {
+    const Drv &d = drv();
+    auto &nv = p->nv;
+    nv.active = false;
+    if (nv.server.joinable()) {
+        if (nv.listen_fd >= 0) shutdown(nv.listen_fd, SHUT_RDWR);
+        nv.server.join();
+    }
+    if (nv.listen_fd >= 0) close(nv.listen_fd), nv.listen_fd = -1;
+    if (nv.export_fd >= 0) close(nv.export_fd), nv.export_fd = -1;
+    if (!d.ok) return;
+    if (nv.mc_va) d.unmap(nv.mc_va, nv.bytes), d.vaFree(nv.mc_va, nv.bytes), nv.mc_va = 0;
+    if (nv.uc_va) d.unmap(nv.uc_va, nv.bytes), d.vaFree(nv.uc_va, nv.bytes), nv.uc_va = 0;
+    if (nv.mapped && nv.mc) {
+        CUdevice dev;
+        if (d.devGet(&dev, nv.device) == CUDA_SUCCESS) d.mcUnbind(nv.mc, dev, 0, nv.bytes);
+    }
+    if (nv.mem) d.release(nv.mem), nv.mem = 0;
+    if (nv.mc) d.release(nv.mc), nv.mc = 0;
+    nv.mapped = nv.joined = false;
+}
+
+static kvq_status nvls_fail(kvq_peer_t p, const std::string &msg, CUresult r) {
+    nvls_release(p);
+    return fail(KVQ_ERR_UNSUPPORTED, msg + " (CUresult " + std::to_string((int)r) + ")");
+}
+
+extern "C" size_t kvq_peer_nvls_handle_bytes(void) { return sizeof(NvlsBlob); }
+
+extern "C" kvq_status kvq_peer_nvls_create(kvq_peer_t p, void *handle_out) {
+    KVQ_REQUIRE(p && handle_out, "kvq_peer_nvls_create: NULL pointer");
+    KVQ_REQUIRE(p->open && !p->nv.joined, "kvq_peer_nvls_create: needs an open peer without NVLS");
+    const Drv &d = drv();
+    if (!d.ok) return fail(KVQ_ERR_UNSUPPORTED, "kvq_peer_nvls_create: driver lacks the multicast API");
+    CUdevice dev;
+    int sup = 0;
+    CUresult r = d.devGet(&dev, p->device);
+    if (r == CUDA_SUCCESS) r = d.devAttr(&sup, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev);
+    if (r != CUDA_SUCCESS || !sup) return fail(KVQ_ERR_UNSUPPORTED, "kvq_peer_nvls_create: device has no multicast support");
+    CUmulticastObjectProp prop{};
+    prop.numDevices = (unsigned)p->nranks;
+    prop.size = (size_t)2 * slot_stride(p->D) * 4;
+    prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR | (p->nranks > 1 ? CU_MEM_HANDLE_TYPE_FABRIC : 0);
+    size_t g = 0;
+    if ((r = d.mcGran(&g, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED)) != CUDA_SUCCESS || g == 0)
+        return nvls_fail(p, "cuMulticastGetGranularity", r);
+    prop.size = (prop.size + g - 1) / g * g;
+    if ((r = d.mcCreate(&p->nv.mc, &prop)) != CUDA_SUCCESS) {
+        prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;  // no fabric handles here: fd only
+        if ((r = d.mcCreate(&p->nv.mc, &prop)) != CUDA_SUCCESS) return nvls_fail(p, "cuMulticastCreate", r);
+    }
+    p->nv.bytes = prop.size;
+    NvlsBlob b{};
+    b.magic = kNvlsMagic;
+    b.size = prop.size;
+    b.nranks = (uint32_t)p->nranks;
+    CUmemFabricHandle fh;
+    if (p->nranks > 1 && (prop.handleTypes & CU_MEM_HANDLE_TYPE_FABRIC) &&
+        d.exportH(&fh, p->nv.mc, CU_MEM_HANDLE_TYPE_FABRIC, 0) == CUDA_SUCCESS) {
+        b.kind = 1;
+        std::memcpy(b.fabric, &fh, sizeof(fh));
+    } else if (p->nranks > 1) {
+        int fd = -1;
+        if ((r = d.exportH(&fd, p->nv.mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0)) != CUDA_SUCCESS)
+            return nvls_fail(p, "cuMemExportToShareableHandle(fd)", r);
+        p->nv.export_fd = fd;
+        b.kind = 2;
+        b.tag = std::random_device{}() ^ ((uint64_t)getpid() << 20) ^ ((uint64_t)std::random_device{}() << 32);
+        p->nv.listen_fd = make_listen(b.tag);
+        if (p->nv.listen_fd < 0) return nvls_fail(p, "abstract unix socket", CUDA_ERROR_UNKNOWN);
+        const int lfd = p->nv.listen_fd, efd = fd, n = p->nranks - 1;
+        p->nv.server = std::thread([lfd, efd, n] {
+            for (int k = 0; k < n; k++) {
+                const int c = accept(lfd, nullptr, nullptr);
+                if (c < 0) return;
+                send_fd(c, efd);
+                close(c);
+            }
+        });
+    } else {
+        b.kind = 0;  // one rank: nothing to share
+    }
+    std::memcpy(handle_out, &b, sizeof(b));
+    return KVQ_OK;
+}
+
+extern "C" kvq_status kvq_peer_nvls_join(kvq_peer_t p, const void *handle) {
+    KVQ_REQUIRE(p && handle, "kvq_peer_nvls_join: NULL pointer");
+    KVQ_REQUIRE(p->open && !p->nv.joined, "kvq_peer_nvls_join: needs an open peer without NVLS");
+    NvlsBlob b;
+    std::memcpy(&b, handle, sizeof(b));
+    KVQ_REQUIRE(b.magic == kNvlsMagic && b.nranks == (uint32_t)p->nranks, "kvq_peer_nvls_join: foreign handle");
+    const Drv &d = drv();
+    if (!d.ok) return fail(KVQ_ERR_UNSUPPORTED, "kvq_peer_nvls_join: driver lacks the multicast API");
+    CUresult r;
+    if (p->rank != 0) {
+        if (b.kind == 1) {
+            CUmemFabricHandle fh;
+            std::memcpy(&fh, b.fabric, sizeof(fh));
+            if ((r = d.importH(&p->nv.mc, &fh, CU_MEM_HANDLE_TYPE_FABRIC)) != CUDA_SUCCESS)
+                return nvls_fail(p, "cuMemImportFromShareableHandle(fabric)", r);
+        } else if (b.kind == 2) {
+            const int fd = recv_fd(b.tag);
+            if (fd < 0) return nvls_fail(p, "receiving the multicast fd", CUDA_ERROR_UNKNOWN);
+            r = d.importH(&p->nv.mc, reinterpret_cast<void *>((uintptr_t)fd), CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+            close(fd);
+            if (r != CUDA_SUCCESS) return nvls_fail(p, "cuMemImportFromShareableHandle(fd)", r);
+        } else {
+            return fail(KVQ_ERR_INVALID_VALUE, "kvq_peer_nvls_join: handle kind");
+        }
+        p->nv.bytes = b.size;
+    }
+    CUdevice dev;
+    if ((r = d.devGet(&dev, p->device)) != CUDA_SUCCESS) return nvls_fail(p, "cuDeviceGet", r);
+    if ((r = d.mcAdd(p->nv.mc, dev)) != CUDA_SUCCESS) return nvls_fail(p, "cuMulticastAddDevice", r);
+    p->nv.device = p->device;
+    p->nv.joined = true;
+    return KVQ_OK;
+}
+
+// Every rank, once every rank has joined (binding and mapping block until all devices are added).
+extern "C" kvq_status kvq_peer_nvls_map(kvq_peer_t p) {
+    KVQ_REQUIRE(p && p->nv.joined && !p->nv.mapped, "kvq_peer_nvls_map: call kvq_peer_nvls_join first");
+    const Drv &d = drv();
+    auto &nv = p->nv;
+    CUmemAllocationProp ap{};
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = nv.device;
+    size_t g = 0;
+    CUresult r = d.memGran(&g, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED);
+    if (r != CUDA_SUCCESS || g == 0 || nv.bytes % g) return nvls_fail(p, "cuMemGetAllocationGranularity", r);
+    if ((r = d.memCreate(&nv.mem, nv.bytes, &ap, 0)) != CUDA_SUCCESS) return nvls_fail(p, "cuMemCreate", r);
+    if ((r = d.mcBind(nv.mc, 0, nv.mem, 0, nv.bytes, 0)) != CUDA_SUCCESS) return nvls_fail(p, "cuMulticastBindMem", r);
+    nv.mapped = true;
+    CUmemAccessDesc acc{};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = nv.device;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    CUdeviceptr va = 0;
+    if ((r = d.vaReserve(&va, nv.bytes, g, 0, 0)) != CUDA_SUCCESS) return nvls_fail(p, "cuMemAddressReserve(mc)", r);
+    if ((r = d.map(va, nv.bytes, 0, nv.mc, 0)) != CUDA_SUCCESS) {
+        d.vaFree(va, nv.bytes);
+        return nvls_fail(p, "cuMemMap(mc)", r);
+    }
+    nv.mc_va = va;
+    if ((r = d.setAccess(va, nv.bytes, &acc, 1)) != CUDA_SUCCESS) return nvls_fail(p, "cuMemSetAccess(mc)", r);
+    va = 0;
+    if ((r = d.vaReserve(&va, nv.bytes, g, 0, 0)) != CUDA_SUCCESS) return nvls_fail(p, "cuMemAddressReserve(uc)", r);
+    if ((r = d.map(va, nv.bytes, 0, nv.mem, 0)) != CUDA_SUCCESS) {
+        d.vaFree(va, nv.bytes);
+        return nvls_fail(p, "cuMemMap(uc)", r);
+    }
+    nv.uc_va = va;
+    if ((r = d.setAccess(va, nv.bytes, &acc, 1)) != CUDA_SUCCESS) return nvls_fail(p, "cuMemSetAccess(uc)", r);
+    if (cudaMemset(reinterpret_cast<void *>(nv.uc_va), 0, nv.bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+        cudaGetLastError();
+        return nvls_fail(p, "zeroing the multicast slots", CUDA_ERROR_UNKNOWN);
+    }
+    return KVQ_OK;
+}
+
+// Every rank, once every rank has mapped: on != 0 routes the a7 exchange through multimem.ld_reduce;
+// on == 0 releases the multicast resources (the P2P slots take over).
+extern "C" kvq_status kvq_peer_nvls_enable(kvq_peer_t p, int on) {
+    KVQ_REQUIRE(p, "kvq_peer_nvls_enable: NULL pointer");
+    if (!on) {
+        cudaDeviceSynchronize();
+        nvls_release(p);
+        return KVQ_OK;
+    }
+    KVQ_REQUIRE(p->nv.mapped && p->nv.mc_va && p->nv.uc_va, "kvq_peer_nvls_enable: call kvq_peer_nvls_map first");
+    p->nv.active = true;
+    return KVQ_OK;
+}
+
+extern "C" int kvq_peer_nvls_active(kvq_peer_t p) { return p && p->nv.active ? 1 : 0; }

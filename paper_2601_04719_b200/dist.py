@@ -24,6 +24,8 @@ def shard_rows(T: int, world: int, rank: int) -> tuple[int, int]:
 def broadcast_bytes(payload: bytes | None, src: int = 0, group=None) -> bytes:
     """Broadcast a short byte string (e.g. a 128-byte ncclUniqueId) from `src`
     to every rank of the default process group (works over gloo and nccl)."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return payload
     obj = [payload]
     dist.broadcast_object_list(obj, src=src, group=group)
     return obj[0]
@@ -73,6 +75,39 @@ def all_ranks_ok(ok: bool) -> bool:
     t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
     return bool(t.item())
+
+
+def enable_nvls(peer, rank: int, world: int) -> bool:
+    """Route the peer's a7 exchange through NVLS multicast (multimem.ld_reduce in the NVSwitch) when every
+    rank can: rank 0 creates the multicast object and broadcasts its handle, every rank joins, then (all
+    joined) maps, then (all mapped) enables.  Any failure anywhere: every rank releases the multicast
+    resources and keeps the P2P exchange.  Returns whether NVLS is active (the same on every rank)."""
+    blob, ok = None, True
+    peer.nvls_reason = ""
+    if rank == 0:
+        try:
+            blob = peer.nvls_create()
+        except Exception as e:  # noqa: BLE001  (no multicast on this device / driver)
+            blob = None
+            peer.nvls_reason = str(e)
+    blob = broadcast_bytes(blob, src=0)
+    ok = blob is not None
+    if ok:
+        try:
+            peer.nvls_join(blob)
+        except Exception as e:  # noqa: BLE001
+            ok = False
+            peer.nvls_reason = str(e)
+    ok = all_ranks_ok(ok)
+    if ok:  # binding blocks until every device has joined: only once all have
+        try:
+            peer.nvls_map()
+        except Exception as e:  # noqa: BLE001
+            ok = False
+            peer.nvls_reason = str(e)
+        ok = all_ranks_ok(ok)
+    peer.nvls_enable(ok)
+    return ok
 
 
 def make_peer(rank: int, world: int, D: int):

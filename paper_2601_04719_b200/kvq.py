@@ -147,6 +147,28 @@ class Peer:
         blob = ctypes.create_string_buffer(b"".join(handles), hb * self.nranks)
         check(load().kvq_peer_open(self.handle, blob), "kvq_peer_open")
 
+    # NVLS (multicast) for the a7 exchange: staged collective setup, see include/kvq.h
+    def nvls_create(self) -> bytes:
+        buf = ctypes.create_string_buffer(load().kvq_peer_nvls_handle_bytes())
+        check(load().kvq_peer_nvls_create(self.handle, buf), "kvq_peer_nvls_create")
+        return buf.raw
+
+    def nvls_join(self, blob: bytes) -> None:
+        n = load().kvq_peer_nvls_handle_bytes()
+        if len(blob) != n:
+            raise ValueError(f"NVLS handle: expected {n} bytes")
+        check(load().kvq_peer_nvls_join(self.handle, ctypes.create_string_buffer(blob, n)), "kvq_peer_nvls_join")
+
+    def nvls_map(self) -> None:
+        check(load().kvq_peer_nvls_map(self.handle), "kvq_peer_nvls_map")
+
+    def nvls_enable(self, on: bool) -> None:
+        check(load().kvq_peer_nvls_enable(self.handle, 1 if on else 0), "kvq_peer_nvls_enable")
+
+    @property
+    def nvls_active(self) -> bool:
+        return bool(load().kvq_peer_nvls_active(self.handle))
+
     def destroy(self):
         if self.handle:
             check(load().kvq_peer_destroy(self.handle), "kvq_peer_destroy")

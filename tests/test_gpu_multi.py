@@ -8,6 +8,8 @@ checked against the CPU oracle.  Collected everywhere; skipped unless at least `
   over the ranks) agree with the oracle's L2 / max-abs / attention error.
 * C4 (131072 x 8192) at the largest world: scales equal the SURVEY appendix golden, every rank's codes and
   K_hat equal the oracle's on its own rows (chunked), L2 / max-abs agree with the goldens.
+* "nvls": the peer exchange with the a7 max read through NVLS multicast (multimem.ld_reduce in the NVSwitch)
+  when every rank can map it, else every rank keeps P2P (the same results either way).
 * bench.py --gpus N (self-launch under torch.distributed.run) prints one line with n_gpus = N for both
   communicators, and the two give the same fidelity metrics.
 """
@@ -39,7 +41,7 @@ SHARE = os.environ.get("KVQ_TEST_SHARE_GPU") == "1"  # harness check on one GPU:
 
 
 def _need(world, comm_kind="nccl"):
-    if NGPU >= world or (SHARE and NGPU >= 1 and comm_kind == "peer"):
+    if NGPU >= world or (SHARE and NGPU >= 1 and comm_kind in ("peer", "nvls")):
         return
     pytest.skip(f"needs {world} GPUs, {NGPU} visible")
 
@@ -57,7 +59,7 @@ def _rank_main(rank, world, port, out_dir, comm_kind, cfg, check_rows):
         import torch.distributed as dist
 
         from paper_2601_04719_b200 import kvq
-        from paper_2601_04719_b200.dist import make_comm, make_peer, shard_rows
+        from paper_2601_04719_b200.dist import enable_nvls, make_comm, make_peer, shard_rows
         dev = torch.device("cuda", rank % torch.cuda.device_count())
         torch.cuda.set_device(dev)
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
@@ -66,8 +68,11 @@ def _rank_main(rank, world, port, out_dir, comm_kind, cfg, check_rows):
         K = kvq.kvq_synth_fill(rows, D, row0=row0, seed=42, device=dev)
         Q = kvq.kvq_synth_fill(nq, D, seed=43, device=dev)
         peer = None
-        if comm_kind == "peer":
+        nvls = False
+        if comm_kind in ("peer", "nvls"):
             peer = make_peer(rank, world, D)
+            if comm_kind == "nvls":
+                nvls = enable_nvls(peer, rank, world)  # False: no multicast here, the P2P exchange is kept
             comm = kvq.Comm.from_peer(peer)
         else:
             comm = make_comm(rank, world)
@@ -81,6 +86,7 @@ def _rank_main(rank, world, port, out_dir, comm_kind, cfg, check_rows):
         torch.cuda.synchronize()
         same = bool(torch.equal(q, q2) and torch.equal(kh.view(torch.int32), kh2.view(torch.int32)))
         res = dict(scales=s.cpu().numpy(), same=np.array(same), row0=np.array(row0), rows=np.array(rows),
+                   nvls=np.array(nvls),
                    metrics=np.array([m["l2"], m["max_abs"], m["attn_mean_abs"]]),
                    metrics2=np.array([m2["l2"], m2["max_abs"], m2["attn_mean_abs"]]))
         if check_rows:
@@ -132,7 +138,7 @@ def _run(world, comm_kind, cfg, tmp_path, check_rows=0, timeout=900):
 
 
 @pytest.mark.timeout(1200)
-@pytest.mark.parametrize("comm_kind", ["nccl", "peer"])
+@pytest.mark.parametrize("comm_kind", ["nccl", "peer", "nvls"])
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_sharded_c2_matches_oracle(orc, tmp_path, world, comm_kind):
     _need(world, comm_kind)
@@ -140,6 +146,7 @@ def test_sharded_c2_matches_oracle(orc, tmp_path, world, comm_kind):
     res = _run(world, comm_kind, C2, tmp_path)
     Ko = orc.fill(T, D)
     so, qo, kho = orc.roundtrip(Ko)
+    assert len({bool(r["nvls"]) for r in res}) == 1, "NVLS must be on for all ranks or for none"
     for r in res:
         assert np.array_equal(r["scales"].view(np.uint32), so.view(np.uint32)), "a7: global scales on every rank"
         assert bool(r["same"]), "kvq_roundtrip and the separate calls disagree"
@@ -160,7 +167,7 @@ def test_sharded_c2_matches_oracle(orc, tmp_path, world, comm_kind):
 
 
 @pytest.mark.timeout(2400)
-@pytest.mark.parametrize("comm_kind", ["nccl", "peer"])
+@pytest.mark.parametrize("comm_kind", ["nccl", "peer", "nvls"])
 def test_sharded_c4_matches_goldens_and_oracle(tmp_path, comm_kind):
     world = max(w for w in (2, 4, 8) if w <= max(NGPU, 2))
     _need(world, comm_kind)
