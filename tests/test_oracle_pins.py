@@ -383,3 +383,23 @@ def test_oracle_attn_goldens_file():
         closed = math.sqrt(2 / math.pi) * (1 / 127) * math.sqrt(g["D"] / 36)
         assert g["attn_mean_abs"] == pytest.approx(closed, rel=0.01)
         assert abs(g["attn_mean_abs"] - 0.095) < 0.002
+
+
+@pytest.mark.parametrize("name", ["2^24 x D1024", "2^24 x D8192"])
+def test_c5_goldens_pinned_by_numpy(name):
+    """tests/golden/oracle_c5.json (written by scripts/oracle_c5_goldens.py from oracle/ only) against an
+    independent numpy implementation: the numpy generator (synth_np), Eq. 6 as np.abs(K).max(0) / fp32 127,
+    Eq. 7 as np.clip(np.rint(fp32(K / s)), -127, 127) (IEEE division, half-even), Eq. 8 as fp32 q * s.
+    (The 2^30 entries come from the same oracle code; the GPU suite checks all four.)"""
+    import hashlib
+
+    from synth_np import uniform_np
+    g = gold("oracle_c5.json")[name]
+    K = uniform_np(42, g["T"], g["D"])
+    s = (np.abs(K).max(axis=0) / np.float32(127)).astype(np.float32)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        q = np.where(s > 0, np.clip(np.rint((K / s).astype(np.float32)), -127, 127), 0).astype(np.int8)
+    kh = (q.astype(np.float32) * s).astype(np.float32)
+    assert hashlib.sha256(s.tobytes()).hexdigest() == g["scales_sha256"]
+    assert hashlib.sha256(q.tobytes()).hexdigest() == g["codes_sha256"]
+    assert hashlib.sha256(kh.tobytes()).hexdigest() == g["k_hat_sha256"]
