@@ -206,7 +206,12 @@ kvq_status kvq_quantize_fused(const float *K, int64_t T, int64_t D, float *scale
  * global and bit-identical to kvq_compute_scales over the whole matrix.  Every rank
  * must make the same sequence of calls, and the ranks' kernels must be able to run
  * concurrently (the last CTA waits for its peers).  kvq_peer_destroy: after all ranks'
- * last call has completed (collective, like ncclCommDestroy). */
+ * last call has completed (collective, like ncclCommDestroy).
+ * Argument checks are rank-local: a call that returns an error on one rank enqueues nothing
+ * there, so its peers' exchange kernels wait for a flag that never comes.  The wait is
+ * bounded (KVQ_PEER_TIMEOUT_S, default 120 s): the waiting kernel traps and the peers'
+ * next synchronization reports a launch failure instead of hanging the GPU.  Validate
+ * arguments identically on every rank. */
 size_t kvq_peer_handle_bytes(void);
 /* A communicator whose collectives (the a7 MAX in kvq_compute_scales[_fmt] -- fused into
  * the column-max kernel when D % 4 == 0 and K / scales are 16-byte aligned --, the metric

@@ -134,11 +134,15 @@ extern "C" const char *kvq_status_string(kvq_status s) {
 
 extern "C" const char *kvq_last_error(void) { return g_last_error.c_str(); }
 
-extern "C" kvq_status kvq_device_check(void) { return device_ok(); }
+extern "C" kvq_status kvq_device_check(void) {
+    KVQ_NVTX("kvq_device_check");
+    return device_ok();
+}
 
 // ------------------------------------------------------------------------------ a1 + a2 (+ a7)
 extern "C" kvq_status kvq_compute_scales_fmt(const float *K, int64_t T, int64_t D, float *scales, int fmt,
                                              kvq_comm_t comm, void *stream) {
+    KVQ_NVTX("kvq_compute_scales_fmt");
     KVQ_REQUIRE(K && scales, "kvq_compute_scales: NULL pointer");
     KVQ_REQUIRE(!bad_dims(T, D), "kvq_compute_scales: need T >= 1, D >= 1, T*D <= 2^62");
     KVQ_REQUIRE(fmt == KVQ_FMT_INT8 || fmt == KVQ_FMT_E4M3 || fmt == KVQ_FMT_INT4 || fmt == KVQ_FMT_INT2,
@@ -161,12 +165,14 @@ extern "C" kvq_status kvq_compute_scales_fmt(const float *K, int64_t T, int64_t 
 
 extern "C" kvq_status kvq_compute_scales(const float *K, int64_t T, int64_t D, float *scales, kvq_comm_t comm,
                                          void *stream) {
+    KVQ_NVTX("kvq_compute_scales");
     return kvq_compute_scales_fmt(K, T, D, scales, KVQ_FMT_INT8, comm, stream);
 }
 
 // ------------------------------------------------------------------------------ FP8 E4M3 variant (NEXT-1)
 extern "C" kvq_status kvq_quantize_e4m3(const float *K, const float *scales, int64_t T, int64_t D, uint8_t *Kq8,
                                         float *K_hat, void *stream) {
+    KVQ_NVTX("kvq_quantize_e4m3");
     KVQ_REQUIRE(K && scales && Kq8, "kvq_quantize_e4m3: NULL pointer");
     KVQ_REQUIRE(!bad_dims(T, D), "kvq_quantize_e4m3: need T >= 1, D >= 1, T*D <= 2^62");
     const size_t n = (size_t)(T * D);
@@ -182,6 +188,7 @@ extern "C" kvq_status kvq_quantize_e4m3(const float *K, const float *scales, int
 
 extern "C" kvq_status kvq_dequantize_e4m3(const uint8_t *Kq8, const float *scales, int64_t T, int64_t D,
                                           float *K_hat, void *stream) {
+    KVQ_NVTX("kvq_dequantize_e4m3");
     KVQ_REQUIRE(Kq8 && scales && K_hat, "kvq_dequantize_e4m3: NULL pointer");
     KVQ_REQUIRE(!bad_dims(T, D), "kvq_dequantize_e4m3: need T >= 1, D >= 1, T*D <= 2^62");
     const size_t n = (size_t)(T * D);
@@ -197,6 +204,7 @@ extern "C" size_t kvq_append_workspace_size(int64_t D) { return D < 1 ? 0 : appe
 extern "C" kvq_status kvq_append(const float *K, int64_t T_old, int64_t n_new, int64_t D, uint32_t *absmax,
                                  float *scales, int8_t *Kq, float *K_hat, void *workspace, size_t workspace_bytes,
                                  kvq_comm_t comm, void *stream) {
+    KVQ_NVTX("kvq_append");
     KVQ_REQUIRE(K && absmax && scales && Kq && workspace, "kvq_append: NULL pointer");
     KVQ_REQUIRE(T_old >= 0 && n_new >= 0 && D >= 1, "kvq_append: need T_old >= 0, n_new >= 0, D >= 1");
     const int64_t T = T_old + n_new;
@@ -208,8 +216,12 @@ extern "C" kvq_status kvq_append(const float *K, int64_t T_old, int64_t n_new, i
                 "kvq_append: buffers alias");
     if (K_hat)
         KVQ_REQUIRE(!overlap(K_hat, n * 4, K, n * 4) && !overlap(K_hat, n * 4, Kq, n) &&
-                        !overlap(K_hat, n * 4, scales, d4) && !overlap(K_hat, n * 4, absmax, d4),
+                        !overlap(K_hat, n * 4, scales, d4) && !overlap(K_hat, n * 4, absmax, d4) &&
+                        !overlap(workspace, workspace_bytes, K_hat, n * 4),
                     "kvq_append: K_hat aliases an input");
+    KVQ_REQUIRE(!overlap(workspace, workspace_bytes, K, n * 4) && !overlap(workspace, workspace_bytes, Kq, n) &&
+                    !overlap(workspace, workspace_bytes, scales, d4) && !overlap(workspace, workspace_bytes, absmax, d4),
+                "kvq_append: workspace aliases a buffer");
     KVQ_TRY(device_ok());
     return launch_append(K, T_old, n_new, D, absmax, scales, Kq, K_hat, workspace, comm, (cudaStream_t)stream);
 }
@@ -222,6 +234,7 @@ extern "C" int64_t kvq_packed_row_bytes(int64_t D, int bits) {
 
 extern "C" kvq_status kvq_quantize_packed(const float *K, const float *scales, int64_t T, int64_t D, int bits,
                                           uint8_t *Kp, float *K_hat, void *stream) {
+    KVQ_NVTX("kvq_quantize_packed");
     KVQ_REQUIRE(K && scales && Kp, "kvq_quantize_packed: NULL pointer");
     KVQ_REQUIRE(bits == 4 || bits == 2, "kvq_quantize_packed: bits must be 4 or 2");
     KVQ_REQUIRE(!bad_dims(T, D), "kvq_quantize_packed: need T >= 1, D >= 1, T*D <= 2^62");
@@ -238,6 +251,7 @@ extern "C" kvq_status kvq_quantize_packed(const float *K, const float *scales, i
 
 extern "C" kvq_status kvq_dequantize_packed(const uint8_t *Kp, const float *scales, int64_t T, int64_t D, int bits,
                                             float *K_hat, void *stream) {
+    KVQ_NVTX("kvq_dequantize_packed");
     KVQ_REQUIRE(Kp && scales && K_hat, "kvq_dequantize_packed: NULL pointer");
     KVQ_REQUIRE(bits == 4 || bits == 2, "kvq_dequantize_packed: bits must be 4 or 2");
     KVQ_REQUIRE(!bad_dims(T, D), "kvq_dequantize_packed: need T >= 1, D >= 1, T*D <= 2^62");
@@ -267,17 +281,20 @@ static kvq_status quant_common(const float *K, const float *scales, int64_t T, i
 
 extern "C" kvq_status kvq_quantize(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
                                    void *stream) {
+    KVQ_NVTX("kvq_quantize");
     return quant_common(K, scales, T, D, Kq, nullptr, stream, "kvq_quantize");
 }
 
 extern "C" kvq_status kvq_quantize_dequantize(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
                                               float *K_hat, void *stream) {
+    KVQ_NVTX("kvq_quantize_dequantize");
     KVQ_REQUIRE(K_hat, "kvq_quantize_dequantize: NULL K_hat");
     return quant_common(K, scales, T, D, Kq, K_hat, stream, "kvq_quantize_dequantize");
 }
 
 extern "C" kvq_status kvq_dequantize(const int8_t *Kq, const float *scales, int64_t T, int64_t D, float *K_hat,
                                      void *stream) {
+    KVQ_NVTX("kvq_dequantize");
     KVQ_REQUIRE(Kq && scales && K_hat, "kvq_dequantize: NULL pointer");
     KVQ_REQUIRE(!bad_dims(T, D), "kvq_dequantize: need T >= 1, D >= 1, T*D <= 2^62");
     const size_t n = (size_t)(T * D);
@@ -296,6 +313,7 @@ extern "C" size_t kvq_quantize_fused_workspace_size(int64_t T, int64_t D) {
 extern "C" kvq_status kvq_quantize_fused(const float *K, int64_t T, int64_t D, float *scales, int8_t *Kq,
                                          float *K_hat, void *workspace, size_t workspace_bytes, kvq_comm_t comm,
                                          int *single_pass_out, void *stream) {
+    KVQ_NVTX("kvq_quantize_fused");
     KVQ_REQUIRE(K && scales && Kq && K_hat && workspace, "kvq_quantize_fused: NULL pointer");
     KVQ_REQUIRE(!bad_dims(T, D), "kvq_quantize_fused: need T >= 1, D >= 1, T*D <= 2^62");
     KVQ_REQUIRE(workspace_bytes >= single_pass_workspace_size(D), "kvq_quantize_fused: workspace too small");
@@ -303,7 +321,9 @@ extern "C" kvq_status kvq_quantize_fused(const float *K, int64_t T, int64_t D, f
     KVQ_REQUIRE(!overlap(K, n * 4, Kq, n) && !overlap(K_hat, n * 4, K, n * 4) && !overlap(K_hat, n * 4, Kq, n) &&
                     !overlap(scales, (size_t)D * 4, K, n * 4) && !overlap(scales, (size_t)D * 4, Kq, n) &&
                     !overlap(scales, (size_t)D * 4, K_hat, n * 4) &&
-                    !overlap(workspace, workspace_bytes, K, n * 4),
+                    !overlap(workspace, workspace_bytes, K, n * 4) && !overlap(workspace, workspace_bytes, Kq, n) &&
+                    !overlap(workspace, workspace_bytes, K_hat, n * 4) &&
+                    !overlap(workspace, workspace_bytes, scales, (size_t)D * 4),
                 "kvq_quantize_fused: buffers alias");
     KVQ_TRY(device_ok());
     cudaStream_t s = (cudaStream_t)stream;
@@ -338,6 +358,7 @@ extern "C" kvq_status kvq_error_metrics_async(const float *K, const float *K_hat
                                               const float *Q, int64_t nq, const float *scales, void *workspace,
                                               size_t workspace_bytes, kvq_comm_t comm, kvq_metrics *out_dev,
                                               void *stream) {
+    KVQ_NVTX("kvq_error_metrics_async");
     KVQ_REQUIRE(K && K_hat && workspace && out_dev, "kvq_error_metrics: NULL pointer");
     KVQ_REQUIRE(!bad_dims(T, D), "kvq_error_metrics: need T >= 1, D >= 1, T*D <= 2^62");
     KVQ_REQUIRE(nq >= 0 && (nq == 0 || Q), "kvq_error_metrics: need nq >= 0 and Q when nq > 0");
@@ -357,6 +378,7 @@ extern "C" kvq_status kvq_error_metrics_async(const float *K, const float *K_hat
 extern "C" kvq_status kvq_error_metrics(const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
                                         int64_t nq, const float *scales, void *workspace, size_t workspace_bytes,
                                         kvq_comm_t comm, kvq_metrics *out_host, void *stream) {
+    KVQ_NVTX("kvq_error_metrics");
     KVQ_REQUIRE(out_host, "kvq_error_metrics: NULL out_host");
     KVQ_REQUIRE(workspace && workspace_bytes >= 512 + 64, "kvq_error_metrics: workspace too small");
     // The device copy of the result lives in the last 512 bytes of the workspace.
@@ -377,6 +399,7 @@ extern "C" size_t kvq_roundtrip_workspace_size(int64_t T, int64_t D, int64_t nq)
 extern "C" kvq_status kvq_roundtrip(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
                                     float *K_hat, const float *Q, int64_t nq, void *workspace, size_t workspace_bytes,
                                     kvq_comm_t comm, kvq_metrics *out_dev, void *stream) {
+    KVQ_NVTX("kvq_roundtrip");
     KVQ_REQUIRE(K && scales && Kq && K_hat && workspace && out_dev, "kvq_roundtrip: NULL pointer");
     KVQ_REQUIRE(!bad_dims(T, D), "kvq_roundtrip: need T >= 1, D >= 1, T*D <= 2^62");
     KVQ_REQUIRE(nq >= 0 && (nq == 0 || Q), "kvq_roundtrip: need nq >= 0 and Q when nq > 0");
@@ -405,6 +428,7 @@ extern "C" size_t kvq_step_workspace_size(int64_t T, int64_t D, int64_t nq) {
 extern "C" kvq_status kvq_step(const float *K, int64_t T, int64_t D, const float *Q, int64_t nq, float *scales,
                                int8_t *Kq, float *K_hat, void *workspace, size_t workspace_bytes, kvq_comm_t comm,
                                kvq_metrics *out_dev, void *stream) {
+    KVQ_NVTX("kvq_step");
     KVQ_REQUIRE(K && scales && Kq && K_hat && workspace && out_dev, "kvq_step: NULL pointer");
     KVQ_REQUIRE(!bad_dims(T, D), "kvq_step: need T >= 1, D >= 1, T*D <= 2^62");
     KVQ_REQUIRE(nq >= 0 && (nq == 0 || Q), "kvq_step: need nq >= 0 and Q when nq > 0");
@@ -435,6 +459,7 @@ extern "C" size_t kvq_attention_scores_workspace_size(int64_t D, int64_t nq) {
 extern "C" kvq_status kvq_attention_scores(const float *Q, int64_t nq, const float *K, const float *K_hat, int64_t T,
                                            int64_t D, float *S, void *workspace, size_t workspace_bytes,
                                            void *stream) {
+    KVQ_NVTX("kvq_attention_scores");
     KVQ_REQUIRE(Q && K && S, "kvq_attention_scores: NULL pointer");
     KVQ_REQUIRE(!bad_dims(T, D) && nq >= 1 && nq <= (int64_t(1) << 62) / T, "kvq_attention_scores: bad sizes");
     KVQ_TRY(device_ok());
@@ -450,6 +475,7 @@ extern "C" size_t kvq_scores_from_codes_workspace_size(int64_t D, int64_t nq) {
 extern "C" kvq_status kvq_scores_from_codes(const float *Q, int64_t nq, const int8_t *Kq, const float *scales,
                                             int64_t T, int64_t D, float *S, void *workspace, size_t workspace_bytes,
                                             void *stream) {
+    KVQ_NVTX("kvq_scores_from_codes");
     KVQ_REQUIRE(Q && Kq && scales && S, "kvq_scores_from_codes: NULL pointer");
     KVQ_REQUIRE(!bad_dims(T, D) && nq >= 1 && nq <= (int64_t(1) << 62) / T && nq <= (int64_t(1) << 62) / D,
                 "kvq_scores_from_codes: bad sizes");
@@ -579,6 +605,7 @@ extern "C" kvq_status kvq_roundtrip_host_async(const float *K_host, int64_t T, i
                                                int64_t nq, float *scales_host, int8_t *Kq_host, float *K_hat_host,
                                                kvq_metrics *metrics_host, void *dev_workspace, size_t workspace_bytes,
                                                kvq_comm_t comm, void *stream) {
+    KVQ_NVTX("kvq_roundtrip_host_async");
     return roundtrip_host_enqueue(K_host, T, D, Q_host, nq, scales_host, Kq_host, K_hat_host, metrics_host,
                                   dev_workspace, workspace_bytes, comm, stream, "kvq_roundtrip_host_async");
 }
@@ -587,6 +614,7 @@ extern "C" kvq_status kvq_roundtrip_host(const float *K_host, int64_t T, int64_t
                                          float *scales_host, int8_t *Kq_host, float *K_hat_host,
                                          kvq_metrics *metrics_host, void *dev_workspace, size_t workspace_bytes,
                                          kvq_comm_t comm, void *stream) {
+    KVQ_NVTX("kvq_roundtrip_host");
     KVQ_TRY(roundtrip_host_enqueue(K_host, T, D, Q_host, nq, scales_host, Kq_host, K_hat_host, metrics_host,
                                    dev_workspace, workspace_bytes, comm, stream, "kvq_roundtrip_host"));
     return cuda_check(cudaStreamSynchronize((cudaStream_t)stream), "sync stream");

@@ -123,13 +123,15 @@ __global__ void append_quant_kernel(AppendParams p, int new_rows) {
     phase_quant(p, new_rows != 0, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
 }
 
-size_t append_workspace_size(int64_t D) { return (size_t)D * sizeof(int) + 256; }
+// [n_grown (4 B) | pad to 256 | grown[D] ints] at a 256-byte aligned offset of any caller pointer
+size_t append_workspace_size(int64_t D) { return (size_t)D * sizeof(int) + 256 + 255; }
 
 kvq_status launch_append(const float *K, int64_t T_old, int64_t n_new, int64_t D, uint32_t *absmax, float *scales,
                          int8_t *Kq, float *K_hat, void *ws, kvq_comm_t comm, cudaStream_t s) {
     AppendParams p{K, T_old, n_new, D, absmax, scales, Kq, K_hat, nullptr, nullptr};
-    p.n_grown = reinterpret_cast<int *>(ws);
-    p.grown = reinterpret_cast<int *>(reinterpret_cast<char *>(ws) + 256);
+    char *w = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(ws) + 255) & ~(uintptr_t)255);
+    p.n_grown = reinterpret_cast<int *>(w);  // atomicAdd target: aligned whatever the caller's pointer
+    p.grown = reinterpret_cast<int *>(w + 256);
     const int sms = device_info().num_sms;
     if (!comm && n_new <= kSmallAppend) {
         static int per_sm = [] {

@@ -118,6 +118,7 @@ kvq_status comm_allreduce_metrics(kvq_comm_t comm, double *sums, size_t nsum, ui
 }  // namespace kvq
 
 extern "C" kvq_status kvq_comm_unique_id(void *out_id128) {
+    KVQ_NVTX("kvq_comm_unique_id");
     using namespace kvq;
     if (!out_id128) return fail(KVQ_ERR_INVALID_VALUE, "kvq_comm_unique_id: NULL");
     NcclApi &a = api();
@@ -130,6 +131,7 @@ extern "C" kvq_status kvq_comm_unique_id(void *out_id128) {
 }
 
 extern "C" kvq_status kvq_comm_init(kvq_comm_t *out, const void *id128, int nranks, int rank) {
+    KVQ_NVTX("kvq_comm_init");
     using namespace kvq;
     if (!out || !id128 || nranks < 1 || rank < 0 || rank >= nranks)
         return fail(KVQ_ERR_INVALID_VALUE, "kvq_comm_init: invalid argument");
@@ -150,6 +152,7 @@ extern "C" kvq_status kvq_comm_init(kvq_comm_t *out, const void *id128, int nran
 }
 
 extern "C" kvq_status kvq_comm_from_peer(kvq_comm_t *out, kvq_peer_t p) {
+    KVQ_NVTX("kvq_comm_from_peer");
     using namespace kvq;
     if (!out || !p) return fail(KVQ_ERR_INVALID_VALUE, "kvq_comm_from_peer: NULL");
     if (!peer_ready(p)) return fail(KVQ_ERR_INVALID_VALUE, "kvq_comm_from_peer: call kvq_peer_open first");
@@ -158,6 +161,7 @@ extern "C" kvq_status kvq_comm_from_peer(kvq_comm_t *out, kvq_peer_t p) {
 }
 
 extern "C" kvq_status kvq_comm_destroy(kvq_comm_t comm) {
+    KVQ_NVTX("kvq_comm_destroy");
     using namespace kvq;
     if (!comm) return KVQ_OK;
     if (comm->peer) {  // the peer itself belongs to the caller (kvq_peer_destroy)

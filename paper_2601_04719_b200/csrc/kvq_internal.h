@@ -10,7 +10,19 @@
 
 #include "../../include/kvq.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace kvq {
+
+// NVTX range around every C-ABI call (header-only NVTX v3: a no-op unless a profiler injects itself), so
+// nsys / ncu timelines show which ABI call enqueued which kernels.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+#define KVQ_NVTX(name) ::kvq::NvtxRange kvq_nvtx_range_(name)
 
 // Thread-local last-error message (kvq_last_error).
 void set_error(const std::string &msg);

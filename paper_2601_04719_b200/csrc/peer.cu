@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <random>
@@ -52,6 +53,7 @@ struct PeerArgs {
     int64_t D, slot_stride;    // u32 per slot (D rounded up to 64)
     uint64_t epoch;
     float divisor;
+    uint64_t timeout_ns;       // a peer that has not arrived by then failed or died: trap instead of hanging
 };
 
 // exchange buffer layout (u32 units): [flags: kPeerMax x u64 = 32 u32][ticket: 1 u32, pad to 64]
@@ -105,8 +107,19 @@ __device__ __forceinline__ void peer_signal_wait(const PeerArgs &pa) {
             st_release_sys(reinterpret_cast<uint64_t *>(pa.bufs[r]) + pa.rank, pa.epoch);
     }
     const uint64_t *flags = reinterpret_cast<const uint64_t *>(pa.bufs[pa.rank]);
-    if ((int)threadIdx.x < pa.nranks)
-        while (ld_acquire_sys(flags + threadIdx.x) < pa.epoch) __nanosleep(32);
+    if ((int)threadIdx.x < pa.nranks) {
+        uint64_t t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while (ld_acquire_sys(flags + threadIdx.x) < pa.epoch) {
+            __nanosleep(32);
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            // Bounded wait: a rank that returned an error before its exchange (argument checks are
+            // rank-local) or died never raises its flag.  Fail loudly (the caller's next synchronization
+            // reports a launch failure) instead of spinning forever.
+            if (t - t0 > pa.timeout_ns) __trap();
+        }
+    }
     __syncthreads();
     fence_acq_rel_sys();
 }
@@ -283,6 +296,7 @@ using namespace kvq;
 extern "C" size_t kvq_peer_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
 
 extern "C" kvq_status kvq_peer_init(kvq_peer_t *out, int nranks, int rank, int64_t D, void *handle_out) {
+    KVQ_NVTX("kvq_peer_init");
     KVQ_REQUIRE(out && handle_out, "kvq_peer_init: NULL pointer");
     KVQ_REQUIRE(nranks >= 1 && nranks <= kPeerMax && rank >= 0 && rank < nranks,
                 "kvq_peer_init: need 1 <= nranks <= 16 and 0 <= rank < nranks");
@@ -317,6 +331,7 @@ extern "C" kvq_status kvq_peer_init(kvq_peer_t *out, int nranks, int rank, int64
 }
 
 extern "C" kvq_status kvq_peer_open(kvq_peer_t p, const void *handles) {
+    KVQ_NVTX("kvq_peer_open");
     KVQ_REQUIRE(p && handles, "kvq_peer_open: NULL pointer");
     KVQ_REQUIRE(!p->open, "kvq_peer_open: already open");
     for (int r = 0; r < p->nranks; r++) {
@@ -342,6 +357,7 @@ extern "C" kvq_status kvq_peer_open(kvq_peer_t p, const void *handles) {
 static void nvls_release(kvq_peer_t p);
 
 extern "C" kvq_status kvq_peer_destroy(kvq_peer_t p) {
+    KVQ_NVTX("kvq_peer_destroy");
     if (!p) return KVQ_OK;
     cudaDeviceSynchronize();
     nvls_release(p);
@@ -367,6 +383,12 @@ static PeerArgs peer_args(kvq_peer_t p, float divisor) {
     pa.slot_stride = slot_stride(p->D);
     pa.epoch = ++p->epoch;
     pa.divisor = divisor;
+    static const uint64_t timeout_ns = [] {
+        const char *e = std::getenv("KVQ_PEER_TIMEOUT_S");  // default 120 s
+        const double sec = e ? std::atof(e) : 120.0;
+        return (uint64_t)((sec > 0 ? sec : 120.0) * 1e9);
+    }();
+    pa.timeout_ns = timeout_ns;
     return pa;
 }
 
@@ -427,6 +449,7 @@ kvq_status peer_compute_scales(const float *K, int64_t T, int64_t D, float *scal
 
 extern "C" kvq_status kvq_compute_scales_peer(const float *K, int64_t T, int64_t D, float *scales, kvq_peer_t p,
                                               void *stream) {
+    KVQ_NVTX("kvq_compute_scales_peer");
     KVQ_REQUIRE((K || T == 0) && scales && p, "kvq_compute_scales_peer: NULL pointer");
     KVQ_REQUIRE(p->open, "kvq_compute_scales_peer: call kvq_peer_open first");
     KVQ_REQUIRE(D == p->D, "kvq_compute_scales_peer: D differs from kvq_peer_init");
@@ -596,6 +619,7 @@ static kvq_status nvls_fail(kvq_peer_t p, const std::string &msg, CUresult r) {
 extern "C" size_t kvq_peer_nvls_handle_bytes(void) { return sizeof(NvlsBlob); }
 
 extern "C" kvq_status kvq_peer_nvls_create(kvq_peer_t p, void *handle_out) {
+    KVQ_NVTX("kvq_peer_nvls_create");
     KVQ_REQUIRE(p && handle_out, "kvq_peer_nvls_create: NULL pointer");
     KVQ_REQUIRE(p->open && !p->nv.joined, "kvq_peer_nvls_create: needs an open peer without NVLS");
     const Drv &d = drv();
@@ -653,6 +677,7 @@ extern "C" kvq_status kvq_peer_nvls_create(kvq_peer_t p, void *handle_out) {
 }
 
 extern "C" kvq_status kvq_peer_nvls_join(kvq_peer_t p, const void *handle) {
+    KVQ_NVTX("kvq_peer_nvls_join");
     KVQ_REQUIRE(p && handle, "kvq_peer_nvls_join: NULL pointer");
     KVQ_REQUIRE(p->open && !p->nv.joined, "kvq_peer_nvls_join: needs an open peer without NVLS");
     NvlsBlob b;
@@ -688,6 +713,7 @@ extern "C" kvq_status kvq_peer_nvls_join(kvq_peer_t p, const void *handle) {
 
 // Every rank, once every rank has joined (binding and mapping block until all devices are added).
 extern "C" kvq_status kvq_peer_nvls_map(kvq_peer_t p) {
+    KVQ_NVTX("kvq_peer_nvls_map");
     KVQ_REQUIRE(p && p->nv.joined && !p->nv.mapped, "kvq_peer_nvls_map: call kvq_peer_nvls_join first");
     const Drv &d = drv();
     auto &nv = p->nv;
@@ -731,6 +757,7 @@ extern "C" kvq_status kvq_peer_nvls_map(kvq_peer_t p) {
 // Every rank, once every rank has mapped: on != 0 routes the a7 exchange through multimem.ld_reduce;
 // on == 0 releases the multicast resources (the P2P slots take over).
 extern "C" kvq_status kvq_peer_nvls_enable(kvq_peer_t p, int on) {
+    KVQ_NVTX("kvq_peer_nvls_enable");
     KVQ_REQUIRE(p, "kvq_peer_nvls_enable: NULL pointer");
     if (!on) {
         cudaDeviceSynchronize();

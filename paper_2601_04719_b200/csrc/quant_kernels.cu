@@ -579,7 +579,9 @@ kvq_status launch_dequantize(const int8_t *Kq, const float *scales, int64_t T, i
 
 namespace kvq {
 
-size_t single_pass_workspace_size(int64_t D) { return (size_t)D * 4 + 256; }
+// D column maxima + the grid barrier word (64 B) at a 256-byte aligned offset of any caller pointer: up to
+// 255 bytes of alignment slack
+size_t single_pass_workspace_size(int64_t D) { return (size_t)D * 4 + 64 + 255; }
 
 // Returns KVQ_ERR_UNSUPPORTED (nothing launched) when the shape or alignment does
 // not allow the single cooperative pass; the caller then runs the two passes.

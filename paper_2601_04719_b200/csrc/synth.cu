@@ -50,6 +50,7 @@ __global__ void synth_kernel(float *__restrict__ out, int64_t row0, int64_t n, i
 
 extern "C" kvq_status kvq_synth_fill(float *out, int64_t row0, int64_t rows, int64_t D, uint64_t seed, int dist,
                                      void *stream) {
+    KVQ_NVTX("kvq_synth_fill");
     using namespace kvq;
     if (!out || rows < 1 || D < 1 || row0 < 0 || dist < 0 || dist > 2)
         return fail(KVQ_ERR_INVALID_VALUE, "kvq_synth_fill: invalid argument");

@@ -228,8 +228,11 @@ def kvq_quantize_e4m3(K: torch.Tensor, scales: torch.Tensor, Kq8: Optional[torch
     _vec(scales, D, "scales")
     if Kq8 is None:
         Kq8 = torch.empty((T, D), dtype=torch.uint8, device=K.device)
+    _out(Kq8, (T, D), torch.uint8, "Kq8")
     if K_hat is None and want_khat:
         K_hat = torch.empty((T, D), dtype=torch.float32, device=K.device)
+    if K_hat is not None:
+        _out(K_hat, (T, D), torch.float32, "K_hat")
     check(load().kvq_quantize_e4m3(_ptr(K), _ptr(scales), T, D, _ptr(Kq8), _ptr(K_hat), _stream(stream)),
           "kvq_quantize_e4m3")
     return (Kq8, K_hat) if K_hat is not None else Kq8
@@ -241,6 +244,7 @@ def kvq_dequantize_e4m3(Kq8: torch.Tensor, scales: torch.Tensor, K_hat: Optional
     _vec(scales, D, "scales")
     if K_hat is None:
         K_hat = torch.empty((T, D), dtype=torch.float32, device=Kq8.device)
+    _out(K_hat, (T, D), torch.float32, "K_hat")
     check(load().kvq_dequantize_e4m3(_ptr(Kq8), _ptr(scales), T, D, _ptr(K_hat), _stream(stream)),
           "kvq_dequantize_e4m3")
     return K_hat
@@ -268,8 +272,10 @@ def kvq_append(K: torch.Tensor, T_old: int, n_new: int, absmax: torch.Tensor, sc
         raise ValueError("K_hat: expected float32 [>= T_old + n_new, D]")
     if workspace is None:
         workspace = torch.empty(kvq_append_workspace_size(D), dtype=torch.uint8, device=K.device)
+    _buf(workspace, kvq_append_workspace_size(D), "workspace")
     check(load().kvq_append(_ptr(K), T_old, n_new, D, _ptr(absmax), _ptr(scales), _ptr(Kq), _ptr(K_hat),
-                            _ptr(workspace), workspace.numel(), _comm_handle(comm), _stream(stream)), "kvq_append")
+                            _ptr(workspace), workspace.numel() * workspace.element_size(), _comm_handle(comm),
+                            _stream(stream)), "kvq_append")
 
 
 class AppendCache:
@@ -318,6 +324,8 @@ def kvq_quantize_packed(K: torch.Tensor, scales: torch.Tensor, bits: int, Kp: Op
         raise ValueError(f"Kp: expected contiguous CUDA uint8[{T}, {rb}]")
     if K_hat is None and want_khat:
         K_hat = torch.empty((T, D), dtype=torch.float32, device=K.device)
+    if K_hat is not None:
+        _out(K_hat, (T, D), torch.float32, "K_hat")
     check(load().kvq_quantize_packed(_ptr(K), _ptr(scales), T, D, bits, _ptr(Kp), _ptr(K_hat), _stream(stream)),
           "kvq_quantize_packed")
     return (Kp, K_hat) if K_hat is not None else Kp
@@ -331,6 +339,7 @@ def kvq_dequantize_packed(Kp: torch.Tensor, scales: torch.Tensor, D: int, bits: 
     _vec(scales, D, "scales")
     if K_hat is None:
         K_hat = torch.empty((T, D), dtype=torch.float32, device=Kp.device)
+    _out(K_hat, (T, D), torch.float32, "K_hat")
     check(load().kvq_dequantize_packed(_ptr(Kp), _ptr(scales), T, D, bits, _ptr(K_hat), _stream(stream)),
           "kvq_dequantize_packed")
     return K_hat
@@ -342,7 +351,7 @@ def kvq_quantize(K: torch.Tensor, scales: torch.Tensor, Kq: Optional[torch.Tenso
     _vec(scales, D, "scales")
     if Kq is None:
         Kq = torch.empty((T, D), dtype=torch.int8, device=K.device)
-    _mat(Kq, torch.int8, "Kq")
+    _out(Kq, (T, D), torch.int8, "Kq")
     check(load().kvq_quantize(_ptr(K), _ptr(scales), T, D, _ptr(Kq), _stream(stream)), "kvq_quantize")
     return Kq
 
@@ -353,7 +362,7 @@ def kvq_dequantize(Kq: torch.Tensor, scales: torch.Tensor, K_hat: Optional[torch
     _vec(scales, D, "scales")
     if K_hat is None:
         K_hat = torch.empty((T, D), dtype=torch.float32, device=Kq.device)
-    _mat(K_hat, torch.float32, "K_hat")
+    _out(K_hat, (T, D), torch.float32, "K_hat")
     check(load().kvq_dequantize(_ptr(Kq), _ptr(scales), T, D, _ptr(K_hat), _stream(stream)), "kvq_dequantize")
     return K_hat
 
@@ -366,6 +375,8 @@ def kvq_quantize_dequantize(K: torch.Tensor, scales: torch.Tensor, Kq: Optional[
         Kq = torch.empty((T, D), dtype=torch.int8, device=K.device)
     if K_hat is None:
         K_hat = torch.empty((T, D), dtype=torch.float32, device=K.device)
+    _out(Kq, (T, D), torch.int8, "Kq")
+    _out(K_hat, (T, D), torch.float32, "K_hat")
     check(load().kvq_quantize_dequantize(_ptr(K), _ptr(scales), T, D, _ptr(Kq), _ptr(K_hat), _stream(stream)),
           "kvq_quantize_dequantize")
     return Kq, K_hat
@@ -383,12 +394,16 @@ def kvq_quantize_fused(K: torch.Tensor, scales: Optional[torch.Tensor] = None, K
         Kq = torch.empty((T, D), dtype=torch.int8, device=K.device)
     if K_hat is None:
         K_hat = torch.empty((T, D), dtype=torch.float32, device=K.device)
+    _out(Kq, (T, D), torch.int8, "Kq")
+    _out(K_hat, (T, D), torch.float32, "K_hat")
     need = int(load().kvq_quantize_fused_workspace_size(T, D))
     if workspace is None:
         workspace = torch.empty(need, dtype=torch.uint8, device=K.device)
+    _buf(workspace, need, "workspace")
     flag = ctypes.c_int(0)
     check(load().kvq_quantize_fused(_ptr(K), T, D, _ptr(scales), _ptr(Kq), _ptr(K_hat), _ptr(workspace),
-                                    workspace.numel(), _comm_handle(comm), ctypes.byref(flag), _stream(stream)),
+                                    workspace.numel() * workspace.element_size(), _comm_handle(comm), ctypes.byref(flag),
+                                    _stream(stream)),
           "kvq_quantize_fused")
     return scales, Kq, K_hat, bool(flag.value)
 
@@ -399,17 +414,18 @@ def kvq_error_metrics_workspace_size(T: int, D: int, nq: int) -> int:
 
 def _metrics_args(K, K_hat, Q, scales, workspace):
     T, D = _mat(K, torch.float32, "K")
-    _mat(K_hat, torch.float32, "K_hat")
+    _out(K_hat, (T, D), torch.float32, "K_hat")
     nq = 0
     if Q is not None:
         nq, Dq = _mat(Q, torch.float32, "Q")
-        assert Dq == D
+        if Dq != D:
+            raise ValueError("Q: expected D columns")
     if scales is not None:
         _vec(scales, D, "scales")
     need = kvq_error_metrics_workspace_size(T, D, nq)
     if workspace is None:
         workspace = torch.empty(need, dtype=torch.uint8, device=K.device)
-    assert workspace.numel() >= need, "workspace too small"
+    _buf(workspace, need, "workspace")
     return T, D, nq, workspace
 
 
@@ -419,8 +435,9 @@ def kvq_error_metrics_async(K, K_hat, Q=None, scales=None, out_dev: Optional[tor
     T, D, nq, workspace = _metrics_args(K, K_hat, Q, scales, workspace)
     if out_dev is None:
         out_dev = torch.empty(METRICS_BYTES, dtype=torch.uint8, device=K.device)
+    _buf(out_dev, METRICS_BYTES, "out_dev")
     check(load().kvq_error_metrics_async(_ptr(K), _ptr(K_hat), T, D, _ptr(Q), nq, _ptr(scales), _ptr(workspace),
-                                         workspace.numel(), _comm_handle(comm), _ptr(out_dev), _stream(stream)),
+                                         workspace.numel() * workspace.element_size(), _comm_handle(comm), _ptr(out_dev), _stream(stream)),
           "kvq_error_metrics_async")
     return out_dev
 
@@ -436,7 +453,7 @@ def kvq_error_metrics(K, K_hat, Q=None, scales=None, workspace=None, comm: Optio
     T, D, nq, workspace = _metrics_args(K, K_hat, Q, scales, workspace)
     out = kvq_metrics()
     check(load().kvq_error_metrics(_ptr(K), _ptr(K_hat), T, D, _ptr(Q), nq, _ptr(scales), _ptr(workspace),
-                                   workspace.numel(), _comm_handle(comm), ctypes.byref(out), _stream(stream)),
+                                   workspace.numel() * workspace.element_size(), _comm_handle(comm), ctypes.byref(out), _stream(stream)),
           "kvq_error_metrics")
     return out.to_dict()
 
@@ -456,21 +473,24 @@ def kvq_roundtrip(K: torch.Tensor, scales: torch.Tensor, Q: Optional[torch.Tenso
     nq = 0
     if Q is not None:
         nq, Dq = _mat(Q, torch.float32, "Q")
-        assert Dq == D
+        if Dq != D:
+            raise ValueError("Q: expected D columns")
     if Kq is None:
         Kq = torch.empty((T, D), dtype=torch.int8, device=K.device)
     if K_hat is None:
         K_hat = torch.empty((T, D), dtype=torch.float32, device=K.device)
-    _mat(Kq, torch.int8, "Kq")
-    _mat(K_hat, torch.float32, "K_hat")
+    _out(Kq, (T, D), torch.int8, "Kq")
+    _out(K_hat, (T, D), torch.float32, "K_hat")
     need = kvq_roundtrip_workspace_size(T, D, nq)
     if workspace is None:
         workspace = torch.empty(need, dtype=torch.uint8, device=K.device)
-    assert workspace.numel() >= need, "workspace too small"
+    _buf(workspace, need, "workspace")
     if out_dev is None:
         out_dev = torch.empty(METRICS_BYTES, dtype=torch.uint8, device=K.device)
+    _buf(out_dev, METRICS_BYTES, "out_dev")
     check(load().kvq_roundtrip(_ptr(K), _ptr(scales), T, D, _ptr(Kq), _ptr(K_hat), _ptr(Q), nq, _ptr(workspace),
-                               workspace.numel(), _comm_handle(comm), _ptr(out_dev), _stream(stream)),
+                               workspace.numel() * workspace.element_size(), _comm_handle(comm), _ptr(out_dev),
+                               _stream(stream)),
           "kvq_roundtrip")
     return Kq, K_hat, out_dev
 
@@ -512,15 +532,17 @@ def kvq_attention_scores(Q: torch.Tensor, K: torch.Tensor, K_hat: Optional[torch
     """workspace="auto" allocates the tensor-core workspace; None selects the CUDA-core kernel."""
     nq, D = _mat(Q, torch.float32, "Q")
     T, D2 = _mat(K, torch.float32, "K")
-    assert D == D2
+    if D != D2:
+        raise ValueError("Q and K: different D")
     if K_hat is not None:
-        _mat(K_hat, torch.float32, "K_hat")
+        _out(K_hat, (T, D), torch.float32, "K_hat")
     if S is None:
         S = torch.empty((nq, T), dtype=torch.float32, device=K.device)
+    _out(S, (nq, T), torch.float32, "S")
     if isinstance(workspace, str):
         workspace = torch.empty(int(load().kvq_attention_scores_workspace_size(D, nq)), dtype=torch.uint8,
                                 device=K.device)
-    nbytes = 0 if workspace is None else workspace.numel()
+    nbytes = 0 if workspace is None else _buf(workspace, 0, "workspace").numel() * workspace.element_size()
     check(load().kvq_attention_scores(_ptr(Q), nq, _ptr(K), _ptr(K_hat), T, D, _ptr(S), _ptr(workspace), nbytes,
                                       _stream(stream)), "kvq_attention_scores")
     return S
@@ -531,14 +553,16 @@ def kvq_scores_from_codes(Q: torch.Tensor, Kq: torch.Tensor, scales: torch.Tenso
     """S[i][t] = sum_d Q[i][d] * Kq[t][d] * scales[d] from the int8 codes (tensor cores when eligible)."""
     nq, D = _mat(Q, torch.float32, "Q")
     T, D2 = _mat(Kq, torch.int8, "Kq")
-    assert D == D2
+    if D != D2:
+        raise ValueError("Q and Kq: different D")
     _vec(scales, D, "scales")
     if S is None:
         S = torch.empty((nq, T), dtype=torch.float32, device=Kq.device)
+    _out(S, (nq, T), torch.float32, "S")
     if isinstance(workspace, str):
         workspace = torch.empty(int(load().kvq_scores_from_codes_workspace_size(D, nq)), dtype=torch.uint8,
                                 device=Kq.device)
-    nbytes = 0 if workspace is None else workspace.numel()
+    nbytes = 0 if workspace is None else _buf(workspace, 0, "workspace").numel() * workspace.element_size()
     check(load().kvq_scores_from_codes(_ptr(Q), nq, _ptr(Kq), _ptr(scales), T, D, _ptr(S), _ptr(workspace), nbytes,
                                        _stream(stream)), "kvq_scores_from_codes")
     return S
@@ -559,13 +583,20 @@ def kvq_roundtrip_host(K_host: torch.Tensor, Q_host: Optional[torch.Tensor] = No
         scales_host = torch.empty(D, dtype=torch.float32, pin_memory=K_host.is_pinned())
     if Kq_host is None:
         Kq_host = torch.empty((T, D), dtype=torch.int8, pin_memory=K_host.is_pinned())
+    # host outputs the library writes with device-to-host copies: exact size and dtype (an undersized host
+    # buffer would be overrun silently)
+    _out(scales_host, (D,), torch.float32, "scales_host", cuda=False)
+    _out(Kq_host, (T, D), torch.int8, "Kq_host", cuda=False)
+    if K_hat_host is not None:
+        _out(K_hat_host, (T, D), torch.float32, "K_hat_host", cuda=False)
     need = kvq_roundtrip_host_workspace_size(T, D, nq)
     if workspace is None:
         workspace = torch.empty(need, dtype=torch.uint8, device=device)
-    assert workspace.numel() >= need
+    _buf(workspace, need, "workspace")
     m = kvq_metrics()
     check(load().kvq_roundtrip_host(_ptr(K_host), T, D, _ptr(Q_host), nq, _ptr(scales_host), _ptr(Kq_host),
-                                    _ptr(K_hat_host), ctypes.byref(m), _ptr(workspace), workspace.numel(),
+                                    _ptr(K_hat_host), ctypes.byref(m), _ptr(workspace),
+                                    workspace.numel() * workspace.element_size(),
                                     _comm_handle(comm), _stream(stream)), "kvq_roundtrip_host")
     return {"scales": scales_host, "Kq": Kq_host, "K_hat": K_hat_host, "metrics": m.to_dict()}
 
@@ -580,9 +611,17 @@ def kvq_roundtrip_host_async(K_host: torch.Tensor, Q_host: Optional[torch.Tensor
     for t in (K_host, scales_host, Kq_host, metrics_host) + ((Q_host,) if Q_host is not None else ()):
         if not t.is_pinned():
             raise ValueError("kvq_roundtrip_host_async needs pinned host tensors")
-    assert metrics_host.numel() >= METRICS_BYTES and metrics_host.dtype == torch.uint8
+    _out(scales_host, (D,), torch.float32, "scales_host", cuda=False)
+    _out(Kq_host, (T, D), torch.int8, "Kq_host", cuda=False)
+    if K_hat_host is not None:
+        _out(K_hat_host, (T, D), torch.float32, "K_hat_host", cuda=False)
+        if not K_hat_host.is_pinned():
+            raise ValueError("kvq_roundtrip_host_async needs pinned host tensors")
+    _buf(metrics_host, METRICS_BYTES, "metrics_host", cuda=False)
+    _buf(workspace, kvq_roundtrip_host_workspace_size(T, D, nq), "workspace")
     check(load().kvq_roundtrip_host_async(_ptr(K_host), T, D, _ptr(Q_host), nq, _ptr(scales_host), _ptr(Kq_host),
-                                          _ptr(K_hat_host), _ptr(metrics_host), _ptr(workspace), workspace.numel(),
+                                          _ptr(K_hat_host), _ptr(metrics_host), _ptr(workspace),
+                                          workspace.numel() * workspace.element_size(),
                                           _comm_handle(comm), _stream(stream)), "kvq_roundtrip_host_async")
 
 
@@ -596,6 +635,6 @@ def kvq_synth_fill(rows: int, D: int, row0: int = 0, seed: int = 42, dist: int =
     if out is None:
         out = torch.empty((rows, D), dtype=torch.float32,
                           device=device or torch.device("cuda", torch.cuda.current_device()))
-    _mat(out, torch.float32, "out")
+    _out(out, (rows, D), torch.float32, "out")
     check(load().kvq_synth_fill(_ptr(out), row0, rows, D, seed, dist, _stream(stream)), "kvq_synth_fill")
     return out

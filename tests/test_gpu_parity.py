@@ -650,3 +650,34 @@ def test_plain_launches_match_pdl_launches(kvq):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(r.stdout.strip().splitlines()[-1])
     assert outs[0] == outs[1], outs
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("target", ["codes", "k_hat", "scales"])
+def test_fault_injection_caught_by_hash_compare(kvq, orc, target):
+    """SURVEY §5 (failure detection): flip ONE byte of an output buffer after the GPU pass and the
+    parity check (SHA-256 against the SURVEY appendix golden for C2, numpy-computed, independent of both
+    paths) must fail; the untouched buffers keep matching.  Guards against a hash compare that passes
+    vacuously."""
+    g = json.load(open(os.path.join(GOLD, "survey_appendix.json")))["C2"]
+    T, D = 8192, 1024
+    K = kvq.kvq_synth_fill(T, D, seed=42)
+    s = kvq.kvq_compute_scales(K)
+    q = kvq.kvq_quantize(K, s)
+    kh = kvq.kvq_dequantize(q, s)
+    bufs = {"scales": s, "codes": q, "k_hat": kh}
+    keys = {"scales": "scales_sha16", "codes": "q_sha16", "k_hat": "khat_sha16"}
+
+    def sha16(t):
+        return hashlib.sha256(host(t).tobytes()).hexdigest()[:16]
+
+    for name, t in bufs.items():
+        assert sha16(t) == g[keys[name]], f"{name} must match before the fault"
+    t = bufs[target]
+    b = t.view(torch.uint8).reshape(-1)
+    pos = b.numel() // 3 + 7
+    b[pos] ^= 0x01  # the injected fault: one bit of one byte, on the device
+    assert sha16(t) != g[keys[target]], "a flipped byte went undetected"
+    for name, u in bufs.items():
+        if name != target:
+            assert sha16(u) == g[keys[name]]
