@@ -241,6 +241,28 @@ def run_reference(args, cfg, rank, world):
 
 
 # ----------------------------------------------------------------------------- the GPU arm
+def plan_tail(ntiles: int, ngrp: int, nsm: int, split_max_pieces: int = 640) -> dict:
+    """The tensor-core pass's tail plan (csrc/attn_tc.cu tc_plan_tail, same cost model), for gpu_launches."""
+    G, W0 = nsm, ntiles // nsm
+    whole = {"split": False, "grid": min(ntiles, nsm), "whole": 0, "rt": 0, "pieces": 1}
+    if W0 < 1:
+        return whole
+    whole_cost = -(-ntiles // G) * ngrp
+    best, bp = float("inf"), whole
+    for W in range(W0, max(0, W0 - 1) - 1, -1):
+        rt = ntiles - W * G
+        if rt <= 0:
+            continue
+        for P in range(2, ngrp + 1):
+            if ngrp % P or rt * P > split_max_pieces:
+                continue
+            np_ = rt * P
+            cost = W * ngrp + (-(-np_ // G)) * (ngrp // P) + 0.9 * np_ / G + 1.5
+            if cost < best:
+                best, bp = cost, {"split": True, "grid": G, "whole": W, "rt": rt, "pieces": P}
+    return bp if bp["split"] and best < 0.97 * whole_cost else whole
+
+
 def launches_per_step(args, comm, comm_kind, rows, D):
     """libkvq kernels one step launches (NCCL's own kernels and memsets not counted), per csrc/:
     scales = colmax + finalize (one fused column-max/exchange/finalize kernel with a peer communicator);
@@ -252,9 +274,7 @@ def launches_per_step(args, comm, comm_kind, rows, D):
     nsm = min(torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count, 160)
     ntiles = (rows + 127) // 128
     ngrp = ((D + 31) // 32 + 3) // 4  # 4-K-block work units per tile (attn_tc.cu)
-    r0 = ntiles % nsm
-    cut = ntiles >= nsm and r0 > 0 and any(ngrp % c == 0 and r0 * c <= nsm for c in range(2, ngrp + 1))
-    combine = 1 if cut else 0  # left-over tiles cut into pieces (attn_tc.cu launch_attn_tc)
+    combine = 1 if plan_tail(ntiles, ngrp, nsm)["split"] else 0  # split tail -> split_combine_kernel
     peer = comm is not None and comm_kind is not None and comm_kind.startswith(("peer", "nvls"))
     scales = 1 if peer else 2
     tail = 0 if comm is None else (2 if peer else 1)

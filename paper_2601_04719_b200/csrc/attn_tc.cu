@@ -146,66 +146,81 @@ struct TcParams {
                          // evict-first loads with normal stores cost ~0.6 GB of extra DRAM reads at C4)
     float *Kh;           // MODE 2: K_hat output [T][D]
     int ngrp;            // work units (groups of CODE_KB K-blocks) per tile row
-    double *split;       // MODE 0, 2: [grid][2][BN][BM] fp64 Delta of tiles split between CTAs (nullptr: whole tiles)
-    int pieces;          // pieces per left-over tile (divides ngrp) when split != nullptr
+    double *split;       // MODE 0, 2: [Rt * pieces][BN][BM] fp64 Delta of the tail pieces (nullptr: whole tiles)
+    int pieces;          // pieces per tail tile (divides ngrp) when split != nullptr
+    int whole;           // with split: whole-tile waves every CTA takes before the tail (W)
+    int rt;              // with split: tail tiles (ntiles - W * grid), each cut into `pieces` K-ranges
 };
 
 // Work distribution.  A work unit is one group of CODE_KB K-blocks (one accumulator chunk, one code
 // box) of one 128-row tile.  Every CTA first takes whole tiles in waves (tile b, b + G, ...: the G CTAs
-// stream G adjacent tiles in lockstep, the write pattern the HBM measured best).  When the R = ntiles mod G
-// tiles left over would leave most SMs idle (R <= G/2), each of them is cut into P equal K-ranges
-// (P | ngrp, R * P <= G) and CTA b takes piece b / R of tile b mod R, so the last wave keeps R * P SMs
-// streaming, still in lockstep.  A cut tile's pieces keep Delta in fp64 and write it to slot 1 (piece 0)
-// or slot 0 (pieces 1..P-1) of their CTA; split_combine_kernel adds the pieces in piece order and takes
-// |Delta|.  Mode 1 (scores) keeps whole tiles only.
+// stream G adjacent tiles in lockstep, the write pattern the HBM measured best).  With a split tail (chosen
+// on the host by a unit-count cost model, see launch_attn_tc) every CTA takes exactly W whole tiles, and the
+// Rt = ntiles - W G tiles left are cut into P equal K-ranges ("pieces" of L = ngrp / P units), numbered
+// piece-major: piece i is K-range i / Rt of tail tile W G + i mod Rt.  CTA b takes pieces b, b + G, b + 2G,
+// ..., so in every round the CTAs work on the same K-range of adjacent tiles (still lockstep).  A piece's
+// Delta goes, in fp64, to its own workspace slot; split_combine_kernel adds the P slots of a tile in piece
+// order and takes |Delta|.  Mode 1 (scores) keeps whole tiles only.
 struct Units {
-    int n, nfull;              // units of this CTA; whole-tile units among them
-    int tail_tile, tail_grp;   // tile and group of the first unit of the tail share
+    int n, nfull;   // units of this CTA; whole-tile units among them
     int G, ngrp;
+    int wbase, rt, L;  // first tail tile (W * G), tail tiles, units per piece
 };
 // Computed once by every thread and broadcast from lane 0 (__shfl_sync), so that the compiler knows
-// the loop state is warp-uniform: the MMA issuer's descriptors then stay in uniform registers (with
-// division results in per-thread registers it re-broadcasts them for every tcgen05.mma).
+// the loop state is warp-uniform: the MMA issuer's descriptors then stay in uniform registers.
 __device__ __forceinline__ Units make_units(const TcParams &p) {
     const int b = blockIdx.x, G = gridDim.x;
-    int n, nfull, tt = 0, tg = 0;
+    int n, nfull, wbase = 0, rt = 0, L = p.ngrp;
     if (!p.split) {
         nfull = n = (p.ntiles - b + G - 1) / G * p.ngrp;
     } else {
-        // left-over tile r = b mod R, piece b / R of P: all CTAs of one piece index start at the same
-        // K-block of adjacent tiles (the lockstep the write stream needs; contiguous shares measured slower)
-        const int W = p.ntiles / G, R = p.ntiles - W * G, P = p.pieces, L = p.ngrp / P;
-        nfull = W * p.ngrp;
-        n = nfull;
-        if (b < R * P) {
-            n += L;
-            tt = W * G + b % R;
-            tg = (b / R) * L;
-        }
+        nfull = p.whole * p.ngrp;
+        wbase = p.whole * G;
+        rt = p.rt;
+        L = p.ngrp / p.pieces;
+        const int np = p.rt * p.pieces;  // tail pieces in all
+        n = nfull + (b < np ? (np - b + G - 1) / G : 0) * L;
     }
     Units us;
     us.n = __shfl_sync(0xffffffffu, n, 0);
     us.nfull = __shfl_sync(0xffffffffu, nfull, 0);
-    us.tail_tile = __shfl_sync(0xffffffffu, tt, 0);
-    us.tail_grp = __shfl_sync(0xffffffffu, tg, 0);
+    us.wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    us.rt = __shfl_sync(0xffffffffu, rt, 0);
+    us.L = __shfl_sync(0xffffffffu, L, 0);
     us.G = G;
     us.ngrp = p.ngrp;
     return us;
 }
-// Walks a CTA's units in order (whole-tile waves, then the tail share) without integer division.
+// Walks a CTA's units in order (whole-tile waves, then its tail pieces); integer division only at piece
+// starts.
 struct UnitWalk {
-    int i, n, nfull, tile, grp, ngrp, G, tail_tile, tail_grp;
+    int i, n, nfull, tile, grp, ngrp, G;
+    int pi, pend, wbase, rt, L;  // current tail piece, its end group; tail geometry
     __device__ __forceinline__ explicit UnitWalk(const Units &u)
-        : i(0), n(u.n), nfull(u.nfull), tile(u.nfull > 0 ? (int)blockIdx.x : u.tail_tile),
-          grp(u.nfull > 0 ? 0 : u.tail_grp), ngrp(u.ngrp), G(u.G), tail_tile(u.tail_tile), tail_grp(u.tail_grp) {}
+        : i(0), n(u.n), nfull(u.nfull), tile((int)blockIdx.x), grp(0), ngrp(u.ngrp), G(u.G), pi((int)blockIdx.x),
+          pend(u.ngrp), wbase(u.wbase), rt(u.rt), L(u.L) {
+        if (nfull == 0 && n > 0) start_piece();
+    }
+    __device__ __forceinline__ void start_piece() {
+        tile = wbase + pi % rt;
+        grp = (pi / rt) * L;
+        pend = grp + L;
+    }
     __device__ __forceinline__ bool ok() const { return i < n; }
+    __device__ __forceinline__ bool in_piece() const { return i >= nfull; }
+    __device__ __forceinline__ bool piece_first() const { return grp == pend - L; }
     __device__ __forceinline__ void next() {
-        if (++i == nfull) {  // whole-tile waves done: continue at the tail share
-            tile = tail_tile;
-            grp = tail_grp;
-        } else if (++grp == ngrp) {
-            grp = 0;
-            tile += i < nfull ? G : 1;
+        ++i;
+        if (i < nfull) {
+            if (++grp == ngrp) {
+                grp = 0;
+                tile += G;
+            }
+        } else if (i == nfull) {
+            start_piece();  // pi == blockIdx.x: the CTA's first tail piece
+        } else if (++grp == pend) {
+            pi += G;
+            start_piece();
         }
     }
 };
@@ -279,25 +294,22 @@ __global__ void __launch_bounds__(256) prep_kernel(const float *__restrict__ Q, 
         colq_body(scales, D, nkb, cq, blockIdx.x - nbq, gridDim.x - nbq);
 }
 
-// Split tiles (see make_units): block (r, y) adds the P pieces of left-over tile r (CTA pc * R + r holds
-// piece pc: slot 1 for pc = 0, slot 0 otherwise) in piece order for queries [16y, 16y + 16), takes |Delta|
-// over the tile's rows < T and queries < nq, and writes the sum as partial G + r * COMBINE_JQ + y.
-// Fixed order throughout: deterministic.
+// Split tail (see make_units): block (r, y) adds the P pieces of tail tile r (slot pc * Rt + r holds K-range
+// pc) in piece order for queries [16y, 16y + 16), takes |Delta| over the tile's rows < T and queries < nq,
+// and writes the sum as partial G + r * COMBINE_JQ + y.  Fixed order throughout: deterministic.
 constexpr int COMBINE_JQ = 4;  // query quarters per tile (blockIdx.y): 4x the loads in flight
-static_assert(kSplitMaxCtas * (1 + COMBINE_JQ) <= 1024, "partials array: max(num_tiles, 1024) entries");
 __global__ void __launch_bounds__(BM) split_combine_kernel(const double *__restrict__ split, int64_t T, int nq,
-                                                           int ntiles, int G, int P, Partial *partials) {
+                                                           int wbase, int rt, int G, int P, Partial *partials) {
     constexpr int JN = BN / COMBINE_JQ;
-    const int rt = blockIdx.x, r = threadIdx.x, j0 = blockIdx.y * JN;
-    const int W = ntiles / G, R = ntiles - W * G;
+    const int r_t = blockIdx.x, r = threadIdx.x, j0 = blockIdx.y * JN;
     pdl_wait();  // the pieces written by the tensor-core pass
     pdl_trigger();
-    const int64_t row = ((int64_t)W * G + rt) * BM + r;
+    const int64_t row = ((int64_t)wbase + r_t) * BM + r;
     double d[JN];
 #pragma unroll
     for (int j = 0; j < JN; j++) d[j] = 0.0;
     for (int pc = 0; pc < P; pc++) {
-        const double *sp = split + ((int64_t)(pc * R + rt) * 2 + (pc > 0 ? 0 : 1)) * (BN * BM) + (int64_t)j0 * BM;
+        const double *sp = split + ((int64_t)pc * rt + r_t) * (BN * BM) + (int64_t)j0 * BM;
 #pragma unroll
         for (int j = 0; j < JN; j++)
             if (j0 + j < nq) d[j] += sp[j * BM + r];
@@ -314,7 +326,7 @@ __global__ void __launch_bounds__(BM) split_combine_kernel(const double *__restr
         if (r < o) red[r] += red[r + o];
         __syncthreads();
     }
-    if (r == 0) partials[G + rt * COMBINE_JQ + blockIdx.y] = Partial{0.0, red[0], 0.0, 0.0};
+    if (r == 0) partials[G + r_t * COMBINE_JQ + blockIdx.y] = Partial{0.0, red[0], 0.0, 0.0};
 }
 
 // byte address of 16-byte chunk c of row r in a [rows][128 B] tile with the TMA 128B swizzle
@@ -687,11 +699,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         double attn = 0.0;
         uint32_t gc = 0;
         [[maybe_unused]] double acc[NTEAMS == 1 ? BN : 1];
-        int piece_grp0 = 0;
         for (UnitWalk w(us); w.ok(); w.next(), gc++) {
             const int tile = w.tile, grp = w.grp;
-            const bool first = grp == 0 || w.i == w.nfull;  // first unit of this CTA's piece of the tile
-            if (first) piece_grp0 = grp;
+            const bool piece = w.in_piece();  // a K-range of a split tail tile (else part of a whole tile)
+            const bool first = piece ? w.piece_first() : grp == 0;
+            const bool last = piece ? grp == w.pend - 1 : grp == ngrp - 1;
             const int ab = gc & 1;
             mbar_wait_sleep(&s.full_acc[ab], (gc >> 1) & 1);
             tc_fence_after();
@@ -746,11 +758,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             tc_fence_before();
             mbar_arrive(&s.empty_acc[ab]);
-            if (w.i != w.n - 1 && grp != ngrp - 1) continue;  // piece not finished
-            const bool whole = piece_grp0 == 0 && grp == ngrp - 1;  // the whole tile row-block is this CTA's
+            if (!last) continue;  // tile / piece not finished
+            const bool whole = !piece;  // the whole tile row-block is this CTA's: Delta is complete
             const int64_t row = (int64_t)tile * BM + r;
-            // a piece of a split tile: slot 0 if it starts inside the tile, else slot 1
-            double *slot = p.split + ((int64_t)blockIdx.x * 2 + (piece_grp0 != 0 ? 0 : 1)) * (BN * BM);
+            // a piece of a split tail tile: its own fp64 slot (piece index w.pi), summed by split_combine_kernel
+            double *slot = piece ? p.split + (int64_t)w.pi * (BN * BM) : nullptr;
 #pragma unroll 1
             for (int hh = 0; hh < (NTEAMS == 1 ? 1 : BN / 8); hh++) {
                 constexpr int NJ = NTEAMS == 1 ? BN : 8;
@@ -855,7 +867,38 @@ size_t tc_colq_bytes(int64_t D) { return (size_t)((D + tc::BK - 1) / tc::BK) * s
 
 size_t tc_split_bytes(int64_t T, int64_t D) {
     const int64_t nunits = (T + tc::BM - 1) / tc::BM * (((D + tc::BK - 1) / tc::BK + tc::CODE_KB - 1) / tc::CODE_KB);
-    return (size_t)std::min<int64_t>(nunits, kSplitMaxCtas) * 2 * tc::BN * tc::BM * sizeof(double);
+    return (size_t)std::min<int64_t>(nunits, kSplitMaxPieces) * tc::BN * tc::BM * sizeof(double);
+}
+
+// Tail plan of the tensor-core pass (see make_units).  Cost model in work units on the critical path: W whole
+// tiles + ceil(Rt P / G) pieces of L units, + 0.9 unit-equivalents per G pieces for the fp64 slots (64 KB
+// written, then read by split_combine: ~0.9 of a unit's 144 KB of K/K_hat/code traffic) + 1.5 units for the
+// combine launch.  Split only after at least one full wave (below that the pieces' slots and the extra launch
+// cost more than they save: C2 and the 8-rank shard measured slower split, profiles/r01/probes/split_time.txt)
+// and only when the model gains >= 3% over whole tiles.  force: -1 auto, 0 whole tiles, 1 the best split.
+TailPlan tc_plan_tail(int ntiles, int ngrp, int nsm, int force) {
+    TailPlan whole{std::min(ntiles, nsm), 0, 0, 1, false};
+    const int G = nsm, W0 = ntiles / G;
+    if (force == 0 || (W0 < 1 && force != 1)) return whole;
+    const double whole_cost = (double)((ntiles + G - 1) / G) * ngrp;
+    double best = 1e300;
+    TailPlan bp = whole;
+    for (int W = W0; W >= std::max(0, W0 - 1); W--) {
+        const int rt = ntiles - W * G;
+        if (rt <= 0) continue;
+        for (int P = 2; P <= ngrp; P++) {
+            if (ngrp % P) continue;
+            const int np = rt * P;
+            if (np > kSplitMaxPieces) continue;
+            const double cost = (double)W * ngrp + (double)((np + G - 1) / G) * (ngrp / P) + 0.9 * np / G + 1.5;
+            if (cost < best) {
+                best = cost;
+                bp = TailPlan{G, W, rt, P, true};
+            }
+        }
+    }
+    if (bp.split && (force == 1 || best < 0.97 * whole_cost)) return bp;
+    return whole;
 }
 
 template <int MODE>
@@ -916,24 +959,20 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
         p.Kh = Kh_out;
     }
     p.ngrp = (int)((nkb + CODE_KB - 1) / CODE_KB);
-    // modes 0/2: whole-tile waves + balanced tail (tiles may be split, see make_units); mode 1: whole tiles
-    // Cut left-over tiles only where whole tiles leave the last wave at most half full after at least one
-    // full wave (the C4 shard at 2 ranks: 512 tiles on 148 SMs = 3 waves + 68 tiles -> 2 pieces each).  One
-    // wave (the 128 tiles of a C4 shard at 8 ranks) and fuller last waves stay whole.
+    // modes 0/2: whole-tile waves + a split tail when the cost model says so (see make_units, tc_plan_tail);
+    // mode 1 (scores): whole tiles
     const int nsm = std::min(device_info().num_sms, kSplitMaxCtas);
-    const int W0 = ntiles / nsm, R0 = W0 ? ntiles % nsm : ntiles;
-    int P = 1;
-    for (int c = 2; R0 > 0 && c <= p.ngrp && R0 * c <= nsm; c++)
-        if (p.ngrp % c == 0) P = c;
-    const char *force = std::getenv("KVQ_TC_BALANCE");  // experiments: 0 = whole tiles, 1 = cut whenever P >= 2
-    const bool want = force ? force[0] == '1' : W0 >= 1;
-    const bool balanced = mode != 1 && ws_split != nullptr && want && P >= 2;
-    const int grid = !balanced ? std::min(ntiles, device_info().num_sms) : (W0 ? nsm : R0 * P);
+    const char *force = std::getenv("KVQ_TC_BALANCE");  // experiments / tests: 0 = whole tiles, 1 = best split
+    const TailPlan plan = tc_plan_tail(ntiles, p.ngrp, nsm, force ? (force[0] == '1' ? 1 : 0) : -1);
+    const bool balanced = mode != 1 && ws_split != nullptr && plan.split;
+    const int grid = balanced ? plan.grid : std::min(ntiles, device_info().num_sms);
     p.split = balanced ? reinterpret_cast<double *>(ws_split) : nullptr;
-    p.pieces = balanced ? P : 1;
-    const int R = balanced ? ntiles - (ntiles / grid) * grid : 0;
+    p.pieces = balanced ? plan.pieces : 1;
+    p.whole = balanced ? plan.whole : 0;
+    p.rt = balanced ? plan.rt : 0;
+    const int R = balanced ? plan.rt : 0;
     const size_t smem = sizeof(Smem);
-    if (grid_out) *grid_out = balanced ? grid + COMBINE_JQ * R : grid;  // + one partial per cut tile and quarter
+    if (grid_out) *grid_out = balanced ? grid + COMBINE_JQ * R : grid;  // + one partial per tail tile and quarter
     if (mode == 0)
         launch_mode<0>(mK, mKh, mKq, p, grid, smem, s);
     else if (mode == 1)
@@ -944,7 +983,7 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
         st != KVQ_OK || !balanced || R == 0)
         return st;
     (void)launch_pdl(split_combine_kernel, dim3(R, COMBINE_JQ), dim3(BM), 0, s, (const double *)p.split, T, (int)nq,
-                     ntiles, grid, P, reinterpret_cast<Partial *>(partials));
+                     plan.whole * grid, plan.rt, grid, plan.pieces, reinterpret_cast<Partial *>(partials));
     return check_launch("attn_tc(split_combine)");
 }
 

@@ -99,9 +99,20 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
                           int64_t nq, void *ws_q, void *partials, int *grid_out, float *S, cudaStream_t s,
                           const float *scales = nullptr, void *ws_colq = nullptr, int8_t *Kq_out = nullptr,
                           float *Kh_out = nullptr, void *ws_split = nullptr);
-// modes 0/2: per-CTA fp64 Delta slots for tiles split between CTAs (at most kSplitMaxCtas CTAs)
+// modes 0/2: fp64 Delta slots for the pieces of a split tail (at most kSplitMaxPieces pieces, grid <= kSplitMaxCtas)
 constexpr int kSplitMaxCtas = 160;
+constexpr int kSplitMaxPieces = 640;
 size_t tc_split_bytes(int64_t T, int64_t D);
+struct TailPlan {
+    int grid, whole, rt, pieces;
+    bool split;
+};
+TailPlan tc_plan_tail(int ntiles, int ngrp, int nsm, int force);
+// the partials array of the metric reductions: per-CTA partials + COMBINE_JQ per tail tile
+inline int64_t metrics_partials_count(int64_t ntiles) {
+    const int64_t a = kSplitMaxCtas + 4 * ntiles;
+    return a > 1024 ? a : 1024;
+}
 // a3+a4+a5+a6 in one pass when eligible, else quantize_dequantize + metrics kernels.
 kvq_status launch_roundtrip_partials(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
                                      float *K_hat, const float *Q, int64_t nq, void *ws, size_t ws_bytes,

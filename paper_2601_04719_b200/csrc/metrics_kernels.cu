@@ -265,7 +265,7 @@ struct WsLayout {
 
 static WsLayout ws_layout(void *ws, int64_t T, int64_t D) {
     const uintptr_t base = (reinterpret_cast<uintptr_t>(ws) + 255) & ~(uintptr_t)255;
-    const size_t np = (size_t)std::max<int64_t>(num_tiles(T), 1024);
+    const size_t np = (size_t)metrics_partials_count(num_tiles(T));
     WsLayout L;
     uintptr_t off = base;
     L.partials = reinterpret_cast<Partial *>(off);
@@ -283,7 +283,7 @@ static WsLayout ws_layout(void *ws, int64_t T, int64_t D) {
 
 size_t metrics_workspace_size(int64_t T, int64_t D, int64_t nq) {
     (void)nq;
-    const size_t np = (size_t)std::max<int64_t>(num_tiles(T), 1024);
+    const size_t np = (size_t)metrics_partials_count(num_tiles(T));
     return 256 + al256(np * sizeof(Partial)) + al256(tc_qsplit_bytes(D)) + al256(tc_colq_bytes(D)) +
            al256(tc_split_bytes(T, D)) + 4 * sizeof(double) + 2 * sizeof(uint64_t);
 }

@@ -37,7 +37,7 @@ NCCL = "nccl (libkvq kvq_comm_t)"
     (131072, object(), PEER, 6),    # fused colmax+exchange+finalize; + metric exchange + metrics_finalize
     (131072, object(), NCCL, 6),    # colmax, finalize, prep, attn, reduce, metrics_finalize (NCCL not counted)
     (65536, object(), PEER, 7),     # 2-rank shard: 512 tiles = 3 waves + 46% -> balanced tail, + split_combine
-    (32768, object(), PEER, 6),     # 4-rank shard: 1.73 waves -> whole tiles
+    (32768, object(), PEER, 7),     # 4-rank shard: 1.73 waves -> 1 whole wave + 108 tiles in 4 pieces, + split_combine
     (16384, object(), PEER, 6),     # 8-rank shard: one wave -> whole tiles
 ])
 def test_fused_step_launch_count(bench, b200, rows, comm, kind, expect):
@@ -86,3 +86,12 @@ def test_cpu_report_per_pass(bench):
     assert r["value"] == 400 * 2 / 4.0
     assert r["full_step_elements_per_s"] == 400 * 2 / 10.0
     assert r["per_pass_s"]["attention"] == 2.5
+
+
+def test_plan_tail_cases(bench):
+    """The tail plan (attn_tc.cu tc_plan_tail) at the C4 shard sizes on 148 SMs (D = 8192: 64 units per tile)."""
+    assert not bench.plan_tail(1024, 64, 148)["split"]                       # 1 rank: 6.92 waves, whole
+    assert bench.plan_tail(512, 64, 148) == {"split": True, "grid": 148, "whole": 3, "rt": 68, "pieces": 2}
+    assert bench.plan_tail(256, 64, 148) == {"split": True, "grid": 148, "whole": 1, "rt": 108, "pieces": 4}
+    assert not bench.plan_tail(128, 64, 148)["split"]                        # 8 ranks: under one wave
+    assert not bench.plan_tail(64, 8, 148)["split"]                          # C2
