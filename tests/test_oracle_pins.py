@@ -403,3 +403,14 @@ def test_c5_goldens_pinned_by_numpy(name):
     assert hashlib.sha256(s.tobytes()).hexdigest() == g["scales_sha256"]
     assert hashlib.sha256(q.tobytes()).hexdigest() == g["codes_sha256"]
     assert hashlib.sha256(kh.tobytes()).hexdigest() == g["k_hat_sha256"]
+
+
+@pytest.mark.parametrize("dist", [1, 2])
+@pytest.mark.parametrize("T,D,row0", [(7, 13, 0), (64, 128, 0), (33, 1000, 5), (1, 4096, 0)])
+def test_structured_generators_match_numpy(orc, dist, T, D, row0):
+    """The oracle's outlier-channel (dist 1) and on-grid (dist 2) generators against independent numpy
+    implementations of the SURVEY §8(c)/(d) recipes (tests/synth_np.py), bit for bit, incl. a shard (row0 > 0)."""
+    from synth_np import ongrid_np, outlier_np
+    want = (outlier_np if dist == 1 else ongrid_np)(42, T, D, row0)
+    got = orc.fill(T, D, 42, dist, row0)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
