@@ -352,8 +352,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (smem_u32(smem_raw) & 1023u) __trap();  // swizzle atoms need 1024-byte alignment
         for (int i = 0; i < Ring<MODE>::kst; i++) {
             mbar_init(&s.full_k[i], 1);
-            mbar_init(&s.empty_k[i], MODE == 2 ? 1 : NCONV_W);  // fused: the store warp frees the stage
-            mbar_init(&s.staged[i], NCONV_W);
+            // every converter thread of the team arrives on the barriers that release shared memory it read
+            // (empty_k in modes 0/1, staged in the fused mode: the K stage and its column records are
+            // overwritten by the next TMA / bulk load after them), so each generic-proxy read is ordered
+            // before the async-proxy overwrite by its own release; full_a (TMEM hand-off) takes one
+            // elected arrival per warp
+            mbar_init(&s.empty_k[i], MODE == 2 ? 1 : NCONV);  // fused: the store warp frees the stage
+            mbar_init(&s.staged[i], NCONV);
         }
         for (int i = 0; i < QST; i++) {
             mbar_init(&s.full_q[i], 1);
@@ -548,8 +553,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         E[2 * c] = f2sub(f2pk(a.x, a.y), f2pk(b.x, b.y));
                         E[2 * c + 1] = f2sub(f2pk(a.z, a.w), f2pk(b.z, b.w));
                     }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&s.empty_k[sk]);
+                    mbar_arrive(&s.empty_k[sk]);
                 } else {
                     // ---- a3 + a4 on the resident K row segment (Eq. 7, Eq. 8); same arithmetic and
                     // exactness argument as quant_v4_kernel (device_common.cuh), two columns per
@@ -632,8 +636,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     KVQ_TR(12, lane == 0 && warp == CONV_W0);
                     fence_proxy_async();  // generic smem writes -> visible to the TMA (async proxy)
                     KVQ_TR(13, lane == 0 && warp == CONV_W0);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&s.staged[sk]);
+                    mbar_arrive(&s.staged[sk]);
                     KVQ_TR(2, lane == 0 && warp == CONV_W0);
                     if (kb == kb1 - 1) cgrp++;
 #pragma unroll

@@ -8,7 +8,10 @@ import torch  # noqa: E402
 from paper_2601_04719_b200 import kvq  # noqa: E402
 
 torch.cuda.set_device(0)
-for (T, D, nq) in [(300, 64, 7), (129, 48, 64), (77, 13, 5), (1, 4, 1), (257, 1024, 64)]:
+for (T, D, nq) in [(300, 64, 7), (129, 48, 64), (77, 13, 5), (1, 4, 1), (257, 1024, 64), (25600, 512, 64)]:
+    # the last shape (200 tiles) runs the tensor-core pass with a split tail (forced): whole waves + pieces
+    if T == 25600:
+        os.environ["KVQ_TC_BALANCE"] = "1"
     K = kvq.kvq_synth_fill(T, D, seed=42, dist=1)
     Q = kvq.kvq_synth_fill(nq, D, seed=43)
     s = kvq.kvq_compute_scales(K)
@@ -33,12 +36,21 @@ for (T, D, nq) in [(300, 64, 7), (129, 48, 64), (77, 13, 5), (1, 4, 1), (257, 10
         assert torch.equal(khb, khb2)
     if nq <= 64:
         Sc = kvq.kvq_scores_from_codes(Q, q, s)
+    # kvq_step: the one-launch small path (cooperative grid barriers) and the two-call path
+    os.environ["KVQ_STEP_SMALL"] = "1"
+    st_s, st_q, st_kh, st_out = kvq.kvq_step(K, Q)
+    os.environ["KVQ_STEP_SMALL"] = "0"
+    st_s2, st_q2, st_kh2, st_out2 = kvq.kvq_step(K, Q)
+    os.environ.pop("KVQ_STEP_SMALL")
+    torch.cuda.synchronize()
+    assert torch.equal(st_q, q) and torch.equal(st_q2, q)
     cache = kvq.AppendCache(T + 8, D)
     cache.append(K[: T // 2])
     cache.append(K[T // 2: T // 2 + 1] * 3.0)
     cache.append(K[T // 2 + 1: T])
     torch.cuda.synchronize()
     print(T, D, nq, "ok", m["attn_mean_abs"], single)
+    os.environ.pop("KVQ_TC_BALANCE", None)
 # peer-memory collectives at world 1 (the exchange kernels, the fused column max + exchange + finalize)
 for D in (64, 13, 1024):
     p = kvq.Peer(1, 0, D)
