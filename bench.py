@@ -245,8 +245,6 @@ def plan_tail(ntiles: int, ngrp: int, nsm: int, split_max_pieces: int = 640) -> 
     """The tensor-core pass's tail plan (csrc/attn_tc.cu tc_plan_tail, same cost model), for gpu_launches."""
     G, W0 = nsm, ntiles // nsm
     whole = {"split": False, "grid": min(ntiles, nsm), "whole": 0, "rt": 0, "pieces": 1}
-    if W0 < 1:
-        return whole
     whole_cost = -(-ntiles // G) * ngrp
     best, bp = float("inf"), whole
     for W in range(W0, max(0, W0 - 1) - 1, -1):

@@ -876,13 +876,13 @@ size_t tc_split_bytes(int64_t T, int64_t D) {
 // Tail plan of the tensor-core pass (see make_units).  Cost model in work units on the critical path: W whole
 // tiles + ceil(Rt P / G) pieces of L units, + 0.9 unit-equivalents per G pieces for the fp64 slots (64 KB
 // written, then read by split_combine: ~0.9 of a unit's 144 KB of K/K_hat/code traffic) + 1.5 units for the
-// combine launch.  Split only after at least one full wave (below that the pieces' slots and the extra launch
-// cost more than they save: C2 and the 8-rank shard measured slower split, profiles/r01/probes/split_time.txt)
-// and only when the model gains >= 3% over whole tiles.  force: -1 auto, 0 whole tiles, 1 the best split.
+// combine launch.  Split only when the model gains >= 3% over whole tiles (C2, 64 tiles of 8 units: 2 pieces
+// each, 55.7 -> 49.8 us per step back to back; the 8-rank C4 shard, 128 tiles of 64 units, stays whole: its
+// split options save no unit on the critical path).  force: -1 auto, 0 whole tiles, 1 the best split.
 TailPlan tc_plan_tail(int ntiles, int ngrp, int nsm, int force) {
     TailPlan whole{std::min(ntiles, nsm), 0, 0, 1, false};
     const int G = nsm, W0 = ntiles / G;
-    if (force == 0 || (W0 < 1 && force != 1)) return whole;
+    if (force == 0) return whole;
     const double whole_cost = (double)((ntiles + G - 1) / G) * ngrp;
     double best = 1e300;
     TailPlan bp = whole;

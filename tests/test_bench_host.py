@@ -94,4 +94,5 @@ def test_plan_tail_cases(bench):
     assert bench.plan_tail(512, 64, 148) == {"split": True, "grid": 148, "whole": 3, "rt": 68, "pieces": 2}
     assert bench.plan_tail(256, 64, 148) == {"split": True, "grid": 148, "whole": 1, "rt": 108, "pieces": 4}
     assert not bench.plan_tail(128, 64, 148)["split"]                        # 8 ranks: under one wave
-    assert not bench.plan_tail(64, 8, 148)["split"]                          # C2
+    assert bench.plan_tail(64, 8, 148) == {"split": True, "grid": 148, "whole": 0, "rt": 64, "pieces": 2}  # C2
+    assert not bench.plan_tail(8, 1, 148)["split"]                           # C1: one unit per tile
