@@ -538,9 +538,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     continue;
                 }
                 const int sk = g % KST;
-                KVQ_TR(14, lane == 0 && warp == CONV_W0);
+                KVQ_TR(14, lane == 0 && (warp - CONV_W0) % NCONV_W == 0);
                 KVQ_WAIT_HOT(&s.full_k[sk], (g / KST) & 1);
-                KVQ_TR(1, lane == 0 && warp == CONV_W0); KVQ_TR(5, lane == 0 && warp == EPI_W0 - 1);
+                KVQ_TR(1, lane == 0 && (warp - CONV_W0) % NCONV_W == 0); KVQ_TR(5, lane == 0 && (warp - CONV_W0) % NCONV_W == NCONV_W - 1);
                 const uint32_t kbase = smem_u32(s.buf + sk * Ring<MODE>::stage);
                 uint64_t E[8];  // E = K - K_hat as fp32 pairs (columns 2j, 2j+1 of this thread's 16)
                 if (MODE != 2) {
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     // K_hat overwrites x in the input stage (same swizzled positions, read by this
                     // thread only); the codes go to the group's code buffer.  The store warp writes
                     // both out with TMA and then frees the stage (and the code buffer).
-                    KVQ_TR(11, lane == 0 && warp == CONV_W0);
+                    KVQ_TR(11, lane == 0 && (warp - CONV_W0) % NCONV_W == 0);
                     if (!code_buf_ready) {
                         KVQ_WAIT_HOT(&s.cstored[cgrp & 1], ((cgrp >> 1) & 1) ^ 1);
                         code_buf_ready = true;
@@ -633,11 +633,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     w.z = pack4(f2lo(V[4]), f2hi(V[4]), f2lo(V[5]), f2hi(V[5]));
                     w.w = pack4(f2lo(V[6]), f2hi(V[6]), f2lo(V[7]), f2hi(V[7]));
                     sts128u(swz(cds, r, (kb % CODE_KB) * 2 + h), w);
-                    KVQ_TR(12, lane == 0 && warp == CONV_W0);
+                    KVQ_TR(12, lane == 0 && (warp - CONV_W0) % NCONV_W == 0);
                     fence_proxy_async();  // generic smem writes -> visible to the TMA (async proxy)
-                    KVQ_TR(13, lane == 0 && warp == CONV_W0);
+                    KVQ_TR(13, lane == 0 && (warp - CONV_W0) % NCONV_W == 0);
                     mbar_arrive(&s.staged[sk]);
-                    KVQ_TR(2, lane == 0 && warp == CONV_W0);
+                    KVQ_TR(2, lane == 0 && (warp - CONV_W0) % NCONV_W == 0);
                     if (kb == kb1 - 1) cgrp++;
 #pragma unroll
                     for (int j = 0; j < 8; j++) E[j] = f2sub(X[j], XH[j]);  // exact (fact 4)
@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 const int sa = g % AST;
                 KVQ_WAIT_HOT(&s.empty_a[sa], ((g / AST) & 1) ^ 1);
-                KVQ_TR(3, lane == 0 && warp == CONV_W0);
+                KVQ_TR(3, lane == 0 && (warp - CONV_W0) % NCONV_W == 0);
                 tc_fence_after();
                 tmem_st16(tbase + lane_off + A_COL0 + sa * 64 + 16 * h, hi);
                 tmem_st16(tbase + lane_off + A_COL0 + sa * 64 + 32 + 16 * h, lo);
@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s.full_a[sa]);
-                KVQ_TR(4, lane == 0 && warp == CONV_W0); KVQ_TR(6, lane == 0 && warp == EPI_W0 - 1);
+                KVQ_TR(4, lane == 0 && (warp - CONV_W0) % NCONV_W == 0); KVQ_TR(6, lane == 0 && (warp - CONV_W0) % NCONV_W == NCONV_W - 1);
             }
         }
         if (MODE != 1) {

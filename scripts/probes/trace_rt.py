@@ -33,8 +33,14 @@ for tiles in [int(x) for x in os.environ.get("TILES", "16,148").split(",")]:
     print("  median period per event:", [int(np.median(np.diff(t[:, e]))) for e in range(11)])
     seq = [14, 1, 11, 12, 13, 2, 3, 4]
     d = [int(np.median(t[:, b] - t[:, a])) for a, b in zip(seq, seq[1:])]
-    d.append(int(np.median(t[1:, 14] - t[:-1, 4])))
-    print("  converter w4 median segments 14>1 1>11 11>12 12>13 13>2 2>3 3>4 4>14':", d)
+    d.append(int(np.median(t[2:, 14] - t[:-2, 4])))
+    print("  converter (first warp of the owning team) median segments 14>1 1>11 11>12 12>13 13>2 2>3 3>4 "
+          "4>14(same team's next block):", d)
+    print("  last warp of the team: full_k seen (5) - first warp (1):", int(np.median(t[:, 5] - t[:, 1])),
+          " full_a arrived (6) - (4):", int(np.median(t[:, 6] - t[:, 4])))
+    print("  load issue -> full_k seen (0>1):", int(np.median(t[:, 1] - t[:, 0])), " 4 -> MMA sees full_a (9):",
+          int(np.median(t[:, 9] - np.maximum(t[:, 4], t[:, 6]))), " MMA 9>10:", int(np.median(t[:, 10] - t[:, 9])),
+          " staged(2) -> store sees (7):", int(np.median(t[:, 7] - t[:, 2])), " 7>8:", int(np.median(t[:, 8] - t[:, 7])))
     ev = [0, 14, 1, 11, 2, 3, 4, 7, 8, 9, 10]
     print("  absolute (cycles from block 64's load issue); events " + " ".join(f"{e:>6d}" for e in ev))
     for g in range(0, 24):
