@@ -89,6 +89,26 @@ __device__ __forceinline__ float4 ld_stream_f4(const float4 *p) {
                  : "l"(p));
     return r;
 }
+// Same, with an L2 eviction-priority policy (createpolicy): evict-first keeps a read-once stream from pushing
+// other lines (e.g. the previous pass's dirty output lines) out of the L2.
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float4 ld_stream_f4_hint(const float4 *p, uint64_t pol) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+// The column-max streams (a1): experiments select the L2 policy (-DKVQ_COLMAX_EF: evict-first hint).
+#ifdef KVQ_COLMAX_EF
+#define KVQ_COLMAX_LD(ptr) ld_stream_f4_hint((ptr), l2_policy_evict_first())
+#else
+#define KVQ_COLMAX_LD(ptr) ld_stream_f4(ptr)
+#endif
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t *p) {
     uint32_t r;
     asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));

@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 6) colmax_peer_kernel(const float4 *
         for (; i + (U - 1) * G < n4; i += U * G) {
             float4 v[U];
 #pragma unroll
-            for (int k = 0; k < U; k++) v[k] = ld_stream_f4(K + i + k * G);
+            for (int k = 0; k < U; k++) v[k] = KVQ_COLMAX_LD(K + i + k * G);
 #pragma unroll
             for (int k = 0; k < U; k++) {
                 m0 = max(m0, absbits(v[k].x));
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 6) colmax_peer_kernel(const float4 *
             }
         }
         for (; i < n4; i += G) {
-            const float4 v = ld_stream_f4(K + i);
+            const float4 v = KVQ_COLMAX_LD(K + i);
             m0 = max(m0, absbits(v.x));
             m1 = max(m1, absbits(v.y));
             m2 = max(m2, absbits(v.z));

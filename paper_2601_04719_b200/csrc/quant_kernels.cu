@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kThreads) colmax_v4_kernel(const float4 *__res
         for (; i + (U - 1) * G < n4; i += U * G) {
             float4 v[U];
 #pragma unroll
-            for (int k = 0; k < U; k++) v[k] = ld_stream_f4(K + i + k * G);
+            for (int k = 0; k < U; k++) v[k] = KVQ_COLMAX_LD(K + i + k * G);
 #pragma unroll
             for (int k = 0; k < U; k++) {
                 m0 = max(m0, absbits(v[k].x));
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(kThreads) colmax_v4_kernel(const float4 *__res
             }
         }
         for (; i < n4; i += G) {
-            float4 v = ld_stream_f4(K + i);
+            float4 v = KVQ_COLMAX_LD(K + i);
             m0 = max(m0, absbits(v.x));
             m1 = max(m1, absbits(v.y));
             m2 = max(m2, absbits(v.z));
