@@ -421,6 +421,27 @@ def run_kvq(args, cfg, rank, world, local_rank):
     else:
         step, pass_names = step_separate, ["scales", "quantize", "dequantize", "metrics"]
 
+    if args.graph:
+        # the whole step captured once into a CUDA graph (PDL edges and the cooperative launch included) and
+        # replayed every step: launch overhead amortized for the launch-bound small configs
+        main_stream, stream = stream, torch.cuda.Stream(device=dev)  # the step closures read `stream`
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                step()
+            stream.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                step()
+        stream = main_stream
+
+        def step(ev=None):  # noqa: F811
+            if ev is not None:
+                ev[0].record(stream)
+            graph.replay()
+            if ev is not None:
+                ev[1].record(stream)
+        pass_names = ["step"]
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -585,7 +606,7 @@ def run_kvq(args, cfg, rank, world, local_rank):
                             ("kvq_compute_scales(a1,a2,+a7 allreduce MAX) -> kvq_roundtrip(a3 quantize, a4 dequantize,"
                              " a5 L2/max, a6 attention error; one HBM pass)") if args.pipeline == "fused" else
                             "kvq_compute_scales -> kvq_quantize -> kvq_dequantize -> kvq_error_metrics_async"),
-                   "pipeline": args.pipeline, "format": args.format,
+                   "pipeline": args.pipeline + (" (CUDA graph)" if args.graph else ""), "format": args.format,
                    "l2_flush": "none needed: inputs larger than L2 (K alone is %.2f GB > 126 MB)" % (4 * T * D / 1e9)
                    if 4 * T * D > 2 * 126e6 else "inputs L2-resident (warm)",
                    "parallelism": f"token-shard x{world}", "comm": comm_kind},
@@ -642,6 +663,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-pass-events", dest="pass_events", action="store_false")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture the step into one CUDA graph and replay it (per-step events around the replay)")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "need >= 3 warm-up steps"
     cfg = dict(CONFIGS[args.config], name=args.config)
