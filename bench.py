@@ -278,6 +278,10 @@ def launches_per_step(args, comm, comm_kind, rows, D):
     tail = 0 if comm is None else (2 if peer else 1)
     if args.format == "int8" and args.pipeline == "step" and comm is None and D <= 256 and rows * D <= (1 << 20):
         return 1  # csrc/step_small.cu: the whole step in one cooperative launch
+    l2 = getattr(torch.cuda.get_device_properties(torch.cuda.current_device()), "L2_cache_size", 0)
+    if (args.format == "int8" and args.pipeline == "step" and comm is None and D % 16 == 0
+            and rows * D * 4 <= l2 // 2):
+        return 3 + combine  # Q split + the tensor-core pass with a1 + a2 fused in front [+ split_combine] + reduce
     if args.format == "int8" and args.pipeline in ("fused", "step"):
         return scales + 3 + combine + tail
     metrics = 3 + combine + tail

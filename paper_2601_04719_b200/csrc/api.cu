@@ -422,7 +422,8 @@ extern "C" kvq_status kvq_roundtrip(const float *K, const float *scales, int64_t
 
 extern "C" size_t kvq_step_workspace_size(int64_t T, int64_t D, int64_t nq) {
     if (bad_dims(T, D) || nq < 0) return 0;
-    return std::max(kvq_roundtrip_workspace_size(T, D, nq), step_small_workspace_size(T, D));
+    return std::max({kvq_roundtrip_workspace_size(T, D, nq), step_small_workspace_size(T, D),
+                     roundtrip_fused_a1_workspace_size(T, D, nq)});
 }
 
 extern "C" kvq_status kvq_step(const float *K, int64_t T, int64_t D, const float *Q, int64_t nq, float *scales,
@@ -447,6 +448,12 @@ extern "C" kvq_status kvq_step(const float *K, int64_t T, int64_t D, const float
     if (step_small_eligible(T, D, nq, comm))
         return launch_step_small(K, T, D, nq ? Q : nullptr, nq, scales, Kq, K_hat, workspace, workspace_bytes,
                                  out_dev, s);
+    if (roundtrip_fused_a1_eligible(K, Kq, K_hat, T, D, nq, comm)) {  // L2-resident K: one cooperative pass
+        MetricTotals tot;
+        tot.fused_out = out_dev;
+        return launch_roundtrip_fused_a1(K, T, D, scales, Kq, K_hat, nq ? Q : nullptr, nq, workspace,
+                                         workspace_bytes, &tot, s);
+    }
     KVQ_TRY(kvq_compute_scales(K, T, D, scales, comm, stream));
     return kvq_roundtrip(K, scales, T, D, Kq, K_hat, Q, nq, workspace, workspace_bytes, comm, out_dev, stream);
 }

@@ -31,6 +31,7 @@
 // D/8 * 3 MMA steps of D = 8192 in TMEM biased |Delta| by ~5e-5 (measured on
 // B200).  Restarting the accumulator every 128 columns (48 MMA steps) and
 // carrying the chunk sums in fp64 keeps the error ~1e-6.
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -150,6 +151,12 @@ struct TcParams {
     int pieces;          // pieces per tail tile (divides ngrp) when split != nullptr
     int whole;           // with split: whole-tile waves every CTA takes before the tail (W)
     int rt;              // with split: tail tiles (ntiles - W * grid), each cut into `pieces` K-ranges
+    // MODE 2 with a1 + a2 fused in front (cooperative launch, kvq_step on L2-resident K): the kernel first
+    // computes the column maxima and the scales itself (pmax != nullptr), then runs the roundtrip
+    uint32_t *pmax;      // [grid][D] per-CTA column maxima (abs bits)
+    const float *Kin;    // K for the column-max phase (generic loads)
+    float *scales_out;   // [D] s_d = fl32(m_d / 127)
+    ColRec *colq_out;    // the per-K-block quantizer records the roundtrip then reads (== colq)
 };
 
 // Work distribution.  A work unit is one group of CODE_KB K-blocks (one accumulator chunk, one code
@@ -329,6 +336,86 @@ __global__ void __launch_bounds__(BM) split_combine_kernel(const double *__restr
     if (r == 0) partials[G + r_t * COMBINE_JQ + blockIdx.y] = Partial{0.0, red[0], 0.0, 0.0};
 }
 
+// a1 + a2 in front of the fused roundtrip (kvq_step on an L2-resident K; cooperative launch, all threads of the
+// CTA, before the warp roles start).  Alg. 1 / Eq. 6 over the CTA's row slab -> its row of partial maxima;
+// grid barrier; Eq. 5/6 for the K-blocks this CTA owns (kb = b, b + G, ...): m_d = max over the partial rows
+// (order-free), s_d = fl32(m_d / 127) (IEEE division), the K-block's quantizer record; grid barrier.  The
+// roundtrip's producer then bulk-loads the records as usual.  `sm` is the (still unused) input ring.
+__device__ __forceinline__ void fused_scales_phase(const TcParams &p, uint8_t *sm) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int b = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
+    const int64_t T = p.T, D = p.D, D4 = D / 4;  // D % 16 == 0 on this path
+    const int64_t r0 = T * b / G, r1 = T * (b + 1) / G;
+    uint32_t *smax = reinterpret_cast<uint32_t *>(sm);  // [D]
+    for (int64_t d = tid; d < D; d += NTHREADS) smax[d] = 0u;
+    __syncthreads();
+    const float4 *K4 = reinterpret_cast<const float4 *>(p.Kin);
+    if (NTHREADS % D4 == 0) {  // column-owning threads: D4 divides the block (D <= 3072)
+        const int rpp = NTHREADS / (int)D4, c4 = tid % (int)D4;
+        uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+        constexpr int U = 8;  // loads in flight per thread
+        for (int64_t r = r0 + tid / (int)D4; r < r1; r += (int64_t)U * rpp) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                v[u] = r + (int64_t)u * rpp < r1 ? __ldcg(K4 + (r + (int64_t)u * rpp) * D4 + c4)  // stays in L2
+                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                m0 = max(m0, absbits(v[u].x));
+                m1 = max(m1, absbits(v[u].y));
+                m2 = max(m2, absbits(v[u].z));
+                m3 = max(m3, absbits(v[u].w));
+            }
+        }
+        atomicMax(&smax[4 * c4 + 0], m0);
+        atomicMax(&smax[4 * c4 + 1], m1);
+        atomicMax(&smax[4 * c4 + 2], m2);
+        atomicMax(&smax[4 * c4 + 3], m3);
+    } else {
+        for (int64_t r = r0; r < r1; r++)
+            for (int64_t c4 = tid; c4 < D4; c4 += NTHREADS) {
+                const float4 v = __ldcg(K4 + r * D4 + c4);
+                atomicMax(&smax[4 * c4 + 0], absbits(v.x));
+                atomicMax(&smax[4 * c4 + 1], absbits(v.y));
+                atomicMax(&smax[4 * c4 + 2], absbits(v.z));
+                atomicMax(&smax[4 * c4 + 3], absbits(v.w));
+            }
+    }
+    __syncthreads();
+    for (int64_t d = tid; d < D; d += NTHREADS) p.pmax[(int64_t)b * D + d] = smax[d];
+    grid.sync();
+    // the K-blocks this CTA owns: warp w of the 24 folds row groups w, w + 24, ... of column `lane`
+    const int lane = tid % 32, wv = tid / 32, nw = NTHREADS / 32;
+    for (int kb = b; kb < p.nkb; kb += G) {
+        __syncthreads();
+        if (tid < 32) smax[tid] = 0u;
+        __syncthreads();
+        const int64_t d = (int64_t)kb * BK + lane;
+        if (d < D) {
+            uint32_t m = 0u;
+            for (int c = wv; c < G; c += nw) m = max(m, __ldcg(p.pmax + (int64_t)c * D + d));
+            atomicMax(&smax[lane], m);
+        }
+        __syncthreads();
+        if (tid < 32) {
+            const float sd = d < D ? __fdiv_rn(__uint_as_float(smax[lane]), 127.0f) : 0.0f;  // Eq. 5/6, Q3
+            const ColQ c = make_colq(sd);
+            p.colq_out[kb].y[lane] = c.y;
+            p.colq_out[kb].s[lane] = sd;
+            const unsigned any = __ballot_sync(0xffffffffu, c.exact);
+            if (lane == 0) {
+                p.colq_out[kb].any_exact = any ? 1u : 0u;
+                p.colq_out[kb].pad[0] = p.colq_out[kb].pad[1] = p.colq_out[kb].pad[2] = 0u;
+            }
+            if (d < D) p.scales_out[d] = sd;
+        }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // the records are read by bulk copies (async proxy)
+    grid.sync();
+}
+
 // byte address of 16-byte chunk c of row r in a [rows][128 B] tile with the TMA 128B swizzle
 __device__ __forceinline__ uint32_t swz(uint32_t base, int r, int c) { return base + r * 128 + ((c ^ (r & 7)) << 4); }
 
@@ -389,6 +476,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // from here on the pass reads Q tiles / column records of the preparation kernel and writes outputs
     pdl_wait();
     pdl_trigger();
+    if constexpr (MODE == 2) {
+        if (p.pmax) fused_scales_phase(p, s.buf);
+    }
     const int ngrp = p.ngrp;
     const Units us = make_units(p);
 
@@ -906,19 +996,36 @@ TailPlan tc_plan_tail(int ntiles, int ngrp, int nsm, int force) {
 
 template <int MODE>
 static void launch_mode(const CUtensorMap &mK, const CUtensorMap &mKh, const CUtensorMap &mKq, const tc::TcParams &p,
-                        int grid, size_t smem, cudaStream_t s) {
+                        int grid, size_t smem, cudaStream_t s, bool cooperative = false) {
     static std::once_flag once;
     std::call_once(once, [&] {
         cudaFuncSetAttribute(tc::attn_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     });
-    (void)launch_pdl(tc::attn_tc_kernel<MODE>, dim3(grid), dim3(tc::NTHREADS), smem, s, mK, mKh, mKq, p);
+    if (!cooperative) {
+        (void)launch_pdl(tc::attn_tc_kernel<MODE>, dim3(grid), dim3(tc::NTHREADS), smem, s, mK, mKh, mKq, p);
+        return;
+    }
+    // grid barriers inside (fused a1 + a2): a cooperative launch guarantees co-residency (1 CTA per SM)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(tc::NTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    (void)cudaLaunchKernelEx(&cfg, tc::attn_tc_kernel<MODE>, mK, mKh, mKq, p);
 }
 
 // Launch: qsplit (into ws_q) [+ colq] + the persistent tensor-core kernel.
 kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
                           int64_t nq, void *ws_q, void *partials, int *grid_out, float *S, cudaStream_t s,
-                          const float *scales, void *ws_colq, int8_t *Kq_out, float *Kh_out, void *ws_split) {
+                          const float *scales, void *ws_colq, int8_t *Kq_out, float *Kh_out, void *ws_split,
+                          float *scales_out, void *ws_pmax) {
     using namespace tc;
+    const bool fused_a1 = mode == 2 && scales_out != nullptr && ws_pmax != nullptr;
     const int64_t nkb = (D + BK - 1) / BK;
     const int ntiles = (int)((T + BM - 1) / BM);
     CUtensorMap mK, mKh, mKq;
@@ -934,7 +1041,7 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
     }
     uint32_t *qs = reinterpret_cast<uint32_t *>(ws_q);
     const unsigned qblocks = (unsigned)std::min<int64_t>((nkb * BN * (BK / 4) + 255) / 256, 4096);
-    if (mode != 2) {
+    if (mode != 2 || fused_a1) {  // (fused a1: the tensor-core kernel writes the column records itself)
         (void)launch_pdl(qsplit_kernel, dim3(qblocks), dim3(256), 0, s, Q, nq, D, nkb, qs);
         if (kvq_status st = check_launch("qsplit"); st != KVQ_OK) return st;
     }
@@ -954,10 +1061,17 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
     }
     if (mode == 2) {
         ColRec *cq = reinterpret_cast<ColRec *>(ws_colq);
-        const unsigned cblocks = (unsigned)std::min<int64_t>((nkb + 7) / 8, 1024);
-        (void)launch_pdl(prep_kernel, dim3(qblocks + cblocks), dim3(256), 0, s, Q, nq, D, nkb, qs, scales, cq,
-                         (int)qblocks);
-        if (kvq_status st = check_launch("qsplit+colq"); st != KVQ_OK) return st;
+        if (fused_a1) {
+            p.pmax = reinterpret_cast<uint32_t *>(ws_pmax);
+            p.Kin = K;
+            p.scales_out = scales_out;
+            p.colq_out = cq;
+        } else {
+            const unsigned cblocks = (unsigned)std::min<int64_t>((nkb + 7) / 8, 1024);
+            (void)launch_pdl(prep_kernel, dim3(qblocks + cblocks), dim3(256), 0, s, Q, nq, D, nkb, qs, scales, cq,
+                             (int)qblocks);
+            if (kvq_status st = check_launch("qsplit+colq"); st != KVQ_OK) return st;
+        }
         p.colq = cq;
         p.Kh = Kh_out;
     }
@@ -981,7 +1095,7 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
     else if (mode == 1)
         launch_mode<1>(mK, mKh, mKq, p, grid, smem, s);
     else
-        launch_mode<2>(mK, mKh, mKq, p, grid, smem, s);
+        launch_mode<2>(mK, mKh, mKq, p, grid, smem, s, fused_a1);
     if (kvq_status st = check_launch(mode == 0 ? "attn_tc(metrics)" : mode == 1 ? "attn_tc(scores)" : "attn_tc(roundtrip)");
         st != KVQ_OK || !balanced || R == 0)
         return st;

@@ -98,7 +98,16 @@ size_t tc_colq_bytes(int64_t D);
 kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
                           int64_t nq, void *ws_q, void *partials, int *grid_out, float *S, cudaStream_t s,
                           const float *scales = nullptr, void *ws_colq = nullptr, int8_t *Kq_out = nullptr,
-                          float *Kh_out = nullptr, void *ws_split = nullptr);
+                          float *Kh_out = nullptr, void *ws_split = nullptr, float *scales_out = nullptr,
+                          void *ws_pmax = nullptr);
+// mode 2 with a1 + a2 fused in front (scales_out, ws_pmax set; cooperative launch): the kvq_step path for an
+// L2-resident K (the pmax workspace holds kSplitMaxCtas x D u32, the largest grid).
+kvq_status launch_roundtrip_fused_a1(const float *K, int64_t T, int64_t D, float *scales_out, int8_t *Kq,
+                                     float *K_hat, const float *Q, int64_t nq, void *ws, size_t ws_bytes,
+                                     MetricTotals *totals, cudaStream_t s);
+size_t roundtrip_fused_a1_workspace_size(int64_t T, int64_t D, int64_t nq);
+bool roundtrip_fused_a1_eligible(const float *K, const int8_t *Kq, const float *K_hat, int64_t T, int64_t D,
+                                 int64_t nq, kvq_comm_t comm);
 // modes 0/2: fp64 Delta slots for the pieces of a split tail (at most kSplitMaxPieces pieces, grid <= kSplitMaxCtas)
 constexpr int kSplitMaxCtas = 160;
 constexpr int kSplitMaxPieces = 640;

@@ -319,6 +319,37 @@ kvq_status launch_metrics_partials(const float *K, const float *K_hat, int64_t T
     return reduce_partials(L, nparts, scales, T, D, nq, totals, s);
 }
 
+// kvq_step on an L2-resident K: a1 + a2 fused into the tensor-core roundtrip (one cooperative launch after the
+// Q split), so the column-max pass, the scale finalize and the column-record prep are not separate kernels and
+// the roundtrip re-reads K from L2.
+size_t roundtrip_fused_a1_workspace_size(int64_t T, int64_t D, int64_t nq) {
+    return metrics_workspace_size(T, D, nq) + 256 + al256((size_t)kSplitMaxCtas * (size_t)D * 4);
+}
+
+bool roundtrip_fused_a1_eligible(const float *K, const int8_t *Kq, const float *K_hat, int64_t T, int64_t D,
+                                 int64_t nq, kvq_comm_t comm) {
+    if (comm || force_simt() || !tc_roundtrip_eligible(K, Kq, K_hat, T, D, nq)) return false;
+    const char *e = std::getenv("KVQ_STEP_FUSED");  // tests / experiments: 0 = never, 1 = whenever eligible
+    if (e) return e[0] == '1';
+    return T * D * 4 <= device_info().l2_bytes / 2;  // K stays in L2 between the column-max phase and the pass
+}
+
+kvq_status launch_roundtrip_fused_a1(const float *K, int64_t T, int64_t D, float *scales_out, int8_t *Kq,
+                                     float *K_hat, const float *Q, int64_t nq, void *ws, size_t ws_bytes,
+                                     MetricTotals *totals, cudaStream_t s) {
+    if (ws_bytes < roundtrip_fused_a1_workspace_size(T, D, nq))
+        return fail(KVQ_ERR_INVALID_VALUE, "kvq_step: workspace too small");
+    const WsLayout L = ws_layout(ws, T, D);
+    const uintptr_t pm = (reinterpret_cast<uintptr_t>(ws) + metrics_workspace_size(T, D, nq) + 255) & ~(uintptr_t)255;
+    int grid = 0;
+    if (kvq_status st = launch_attn_tc(2, K, nullptr, T, D, Q, nq, L.qsplit, L.partials, &grid, nullptr, s,
+                                       scales_out, L.colq, Kq, K_hat, L.split, scales_out,
+                                       reinterpret_cast<void *>(pm));
+        st != KVQ_OK)
+        return st;
+    return reduce_partials(L, grid, scales_out, T, D, nq, totals, s);
+}
+
 kvq_status launch_roundtrip_partials(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
                                      float *K_hat, const float *Q, int64_t nq, void *ws, size_t ws_bytes,
                                      MetricTotals *totals, cudaStream_t s) {

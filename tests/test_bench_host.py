@@ -21,7 +21,8 @@ def bench():
 @pytest.fixture()
 def b200(monkeypatch):
     monkeypatch.setattr(torch.cuda, "current_device", lambda: 0)
-    monkeypatch.setattr(torch.cuda, "get_device_properties", lambda d: types.SimpleNamespace(multi_processor_count=148))
+    monkeypatch.setattr(torch.cuda, "get_device_properties",
+                        lambda d: types.SimpleNamespace(multi_processor_count=148, L2_cache_size=126 << 20))
 
 
 def args(fmt="int8", pipeline="fused"):
@@ -96,3 +97,10 @@ def test_plan_tail_cases(bench):
     assert not bench.plan_tail(128, 64, 148)["split"]                        # 8 ranks: under one wave
     assert bench.plan_tail(64, 8, 148) == {"split": True, "grid": 148, "whole": 0, "rt": 64, "pieces": 2}  # C2
     assert not bench.plan_tail(8, 1, 148)["split"]                           # C1: one unit per tile
+
+
+def test_step_pipeline_launch_counts(bench, b200):
+    a = types.SimpleNamespace(format="int8", pipeline="step")
+    assert bench.launches_per_step(a, None, None, 1024, 128) == 1        # C1: one cooperative launch
+    assert bench.launches_per_step(a, None, None, 8192, 1024) == 4       # C2: qsplit + fused pass + combine + reduce
+    assert bench.launches_per_step(a, None, None, 131072, 8192) == 5     # C4: the two calls

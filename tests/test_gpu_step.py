@@ -160,3 +160,45 @@ def test_rejects_bad_arguments(kvq):
         kvq.kvq_step(K, K_hat=torch.empty(16, 8))  # host output
     with pytest.raises(RuntimeError):  # K_hat aliasing K is refused by the library
         kvq.kvq_step(K, K_hat=K)
+
+
+@pytest.mark.parametrize("T,D,nq", [(8192, 1024, 64), (1000, 48, 64), (300, 8192, 64), (2047, 4096, 17),
+                                    (129, 16, 1), (4096, 256, 0), (20000, 2048, 64)])
+@pytest.mark.parametrize("dist", [0, 1])
+def test_fused_a1_path(kvq, orc, monkeypatch, T, D, nq, dist):
+    """kvq_step with the column max and the scales fused into the tensor-core roundtrip (one cooperative
+    launch after the Q split; the default for L2-resident K such as C2): column-owning (D <= 3072) and
+    generic column-max loops, ragged row slabs, split tails, no queries; uniform and outlier-channel keys."""
+    monkeypatch.setenv("KVQ_STEP_SMALL", "0")
+    monkeypatch.setenv("KVQ_STEP_FUSED", "1")
+    K = orc.fill(T, D, 42, dist)
+    Q = orc.fill(nq, D, 43) if nq else None
+    check(kvq, orc, K, Q, None, None)
+
+
+@pytest.mark.parametrize("name", ["ties", "subnormal", "underflow", "zeros", "mixed"])
+def test_fused_a1_structured(kvq, orc, monkeypatch, name):
+    monkeypatch.setenv("KVQ_STEP_SMALL", "0")
+    monkeypatch.setenv("KVQ_STEP_FUSED", "1")
+    rng = np.random.default_rng(5)
+    T, D = 300, 64
+    if name == "ties":
+        col = np.array([127, 0.5, 1.5, 2.5, -2.5, -127, 63.5, -0.5, 126.5, -126.5], np.float32) / 128
+        K = np.tile(col[:, None], (30, D)).astype(np.float32)
+    elif name == "subnormal":
+        K = (rng.uniform(-1, 1, (T, D)) * 2.0 ** -140).astype(np.float32)
+        K[:, :32] = rng.uniform(-1, 1, (T, 32)).astype(np.float32)
+    elif name == "underflow":
+        K = (rng.choice([-1, 0, 1], (T, D)) * 2.0 ** -149).astype(np.float32)
+    elif name == "zeros":
+        K = np.zeros((T, D), np.float32)
+        K[3, 7] = -2.0
+    else:
+        K = (rng.uniform(-1, 1, (T, D)) * 2.0 ** rng.integers(-60, 60, (1, D))).astype(np.float32)
+    Kd = torch.from_numpy(K).cuda()
+    s, q, kh, out = kvq.kvq_step(Kd, torch.from_numpy(orc.fill(64, D, 43)).cuda())
+    so, qo, kho = orc.roundtrip(K)
+    assert np.array_equal(bits(host(s)), bits(so))
+    assert np.array_equal(bits(host(q)), bits(qo))
+    assert np.array_equal(bits(host(kh)), bits(kho))
+    assert kvq.metrics_from_device(out)["max_abs"] == orc.max_abs_error(K, kho)
