@@ -52,12 +52,15 @@ constexpr int QST = 4, AST = 4;
 // Input ring: modes 0/1 stage K and K_hat (32 KB) x 4; the fused mode stages K only
 // (16 KB) x 8, i.e. 128 KB in flight per SM either way (Little's law at ~44 GB/s/SM).
 constexpr int KST_MAX = 8;
+#ifndef KVQ_TC_KST2
+#define KVQ_TC_KST2 8  // fused-mode ring depth (16 KB stages; experiments: -DKVQ_TC_KST2=4..8)
+#endif
 #ifndef KVQ_TC_KST01
 #define KVQ_TC_KST01 4  // modes 0/1 ring depth (experiments: -DKVQ_TC_KST01=5 fills the 160 KB buffer)
 #endif
 template <int MODE>
 struct Ring {
-    static constexpr int kst = MODE == 2 ? 8 : KVQ_TC_KST01;
+    static constexpr int kst = MODE == 2 ? KVQ_TC_KST2 : KVQ_TC_KST01;
     static constexpr uint32_t stage = MODE == 2 ? 16384u : 32768u;
 };
 // warps: 0 K producer, 1 MMA (+TMEM alloc), 2 output stores (fused mode), 3 Q producer, 4-11 converters (2 per TMEM lane
