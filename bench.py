@@ -270,8 +270,10 @@ def launches_per_step(args, comm, comm_kind, rows, D):
     peer one also its metric-exchange kernel."""
     import torch
     nsm = min(torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count, 160)
-    ntiles = (rows + 127) // 128
-    ngrp = ((D + 31) // 32 + 3) // 4  # 4-K-block work units per tile (attn_tc.cu)
+    if os.environ.get("KVQ_TC_RT64", "0") == "1":  # opt-in 64-row roundtrip kernel (rt64.cuh): units of 4
+        ntiles, ngrp = (rows + 63) // 64, ((((D + 31) // 32 + 1) // 2) + 3) // 4  # stages of 64 columns
+    else:  # the 128-row kernel (attn_tc.cu): 4-K-block work units per tile
+        ntiles, ngrp = (rows + 127) // 128, ((D + 31) // 32 + 3) // 4
     combine = 1 if plan_tail(ntiles, ngrp, nsm)["split"] else 0  # split tail -> split_combine_kernel
     peer = comm is not None and comm_kind is not None and comm_kind.startswith(("peer", "nvls"))
     scales = 1 if peer else 2

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libkvq.so")
 SOURCES = ["api.cu", "quant_kernels.cu", "metrics_kernels.cu", "attn_tc.cu", "fp8_kernels.cu", "lowbit_kernels.cu", "append_kernels.cu", "scores_codes.cu", "step_small.cu", "synth.cu", "peer.cu", "comm.cpp"]
-HEADERS = ["kvq_internal.h", "device_common.cuh", "tc_common.cuh"]
+HEADERS = ["kvq_internal.h", "device_common.cuh", "tc_common.cuh", "rt64.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # IEEE arithmetic everywhere (bit-exact parity needs it): no fast-math, no FTZ,
 # IEEE division/sqrt.  Products that must not be contracted use __fmul_rn etc.

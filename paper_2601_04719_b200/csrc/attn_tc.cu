@@ -101,7 +101,7 @@ struct __align__(16) ColRec {
 
 // Timeline trace of CTA 0 (experiments only, -DKVQ_TRACE): clock64 of event e at K-block g in [TR_G0, TR_G0 + TR_N).
 #ifdef KVQ_TRACE
-constexpr int TR_G0 = 64, TR_N = 64, TR_E = 16;
+constexpr int TR_G0 = 64, TR_N = 64, TR_E = 48;  // events 16..31: each team warp's staged arrival; 32..47: its loads done
 __device__ unsigned long long g_kvq_trace[TR_N][TR_E];
 #define KVQ_TR(e, cond)                                                                            \
     do {                                                                                           \
@@ -681,7 +681,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             XH[j] = f2mul(rr, u ? f2pk(s4.z, s4.w) : f2pk(s4.x, s4.y));
                         }
                     }
+#ifdef KVQ_EXP_NODANGER  // timing experiments only (near-tie quotients not repaired: codes may differ)
+                    if (s.cq[sk].any_exact) {
+#else
                     if (dmax > kDangerThr || amax > 127.25f || s.cq[sk].any_exact) {
+#endif
                         // rare: a near-tie quotient, a quotient past the clamp or an exact-path column ->
                         // the whole segment again with the clamp and, where needed, the IEEE division
 #pragma unroll
@@ -711,6 +715,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     // thread only); the codes go to the group's code buffer.  The store warp writes
                     // both out with TMA and then frees the stage (and the code buffer).
                     KVQ_TR(11, lane == 0 && (warp - CONV_W0) % NCONV_W == 0);
+                    KVQ_TR(32 + (warp - CONV_W0) % NCONV_W, lane == 0);
                     if (!code_buf_ready) {
                         KVQ_WAIT_HOT(&s.cstored[cgrp & 1], ((cgrp >> 1) & 1) ^ 1);
                         code_buf_ready = true;
@@ -731,6 +736,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     KVQ_TR(13, lane == 0 && (warp - CONV_W0) % NCONV_W == 0);
                     mbar_arrive(&s.staged[sk]);
                     KVQ_TR(2, lane == 0 && (warp - CONV_W0) % NCONV_W == 0);
+                    KVQ_TR(16 + (warp - CONV_W0) % NCONV_W, lane == 0);
                     if (kb == kb1 - 1) cgrp++;
 #pragma unroll
                     for (int j = 0; j < 8; j++) E[j] = f2sub(X[j], XH[j]);  // exact (fact 4)
@@ -911,6 +917,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
+}  // namespace tc
+}  // namespace kvq
+#include "rt64.cuh"
+namespace kvq {
+namespace tc {
+
 // ---------------------------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -926,22 +938,29 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// 2-D row-major [T][D] map, box {box_cols, BM rows}, 128B swizzle (box_cols * elem = 128 B).
+// 2-D row-major [T][D] map, box {box_cols, box_rows}, 128B swizzle (box_cols * elem = 128 B).
 static bool make_map(CUtensorMap *m, const void *base, CUtensorMapDataType ty, int elem, int64_t T, int64_t D,
-                     int box_cols) {
+                     int box_cols, int box_rows = BM) {
     auto enc = encode_fn();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)T};
     cuuint64_t strides[1] = {(cuuint64_t)D * elem};
-    cuuint32_t box[2] = {(cuuint32_t)box_cols, BM};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, ty, 2, const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
-static bool make_map_f32(CUtensorMap *m, const float *base, int64_t T, int64_t D) {
-    return make_map(m, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, D, BK);
+static bool make_map_f32(CUtensorMap *m, const float *base, int64_t T, int64_t D, int box_rows = BM) {
+    return make_map(m, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, D, BK, box_rows);
 }
+// KVQ_TC_RT64=1: the fused roundtrip on 64-row tiles (rt64.cuh; parity-green, measured slower: see there).
+static bool use_rt64() {
+    const char *e = std::getenv("KVQ_TC_RT64");
+    return e && e[0] == '1';
+}
+// K-blocks of 32 columns, rounded up to whole 64-column stages (the padded Q tiles and column records are zero)
+static int64_t nkb_padded(int64_t D) { return ((D + BK - 1) / BK + 1) & ~(int64_t)1; }
 
 }  // namespace tc
 
@@ -951,7 +970,7 @@ bool tc_eligible(const float *K, const float *K_hat, int64_t T, int64_t D, int64
            tc::encode_fn() != nullptr;
 }
 
-size_t tc_qsplit_bytes(int64_t D) { return (size_t)((D + tc::BK - 1) / tc::BK) * 2 * tc::QTILE; }
+size_t tc_qsplit_bytes(int64_t D) { return (size_t)tc::nkb_padded(D) * 2 * tc::QTILE; }
 
 bool tc_roundtrip_eligible(const float *K, const int8_t *Kq, const float *K_hat, int64_t T, int64_t D, int64_t nq) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(K) | reinterpret_cast<uintptr_t>(Kq) |
@@ -959,10 +978,13 @@ bool tc_roundtrip_eligible(const float *K, const int8_t *Kq, const float *K_hat,
     return tc_eligible(K, K_hat, T, D, nq) && D % 16 == 0 && (a % 16) == 0;
 }
 
-size_t tc_colq_bytes(int64_t D) { return (size_t)((D + tc::BK - 1) / tc::BK) * sizeof(tc::ColRec); }
+size_t tc_colq_bytes(int64_t D) { return (size_t)tc::nkb_padded(D) * sizeof(tc::ColRec); }
 
 size_t tc_split_bytes(int64_t T, int64_t D) {
-    const int64_t nunits = (T + tc::BM - 1) / tc::BM * (((D + tc::BK - 1) / tc::BK + tc::CODE_KB - 1) / tc::CODE_KB);
+    // work units of either geometry: 128-row tiles x 4 K-blocks, 64-row tiles x 4 stages of 64 columns
+    const int64_t n128 = (T + tc::BM - 1) / tc::BM * (((D + tc::BK - 1) / tc::BK + tc::CODE_KB - 1) / tc::CODE_KB);
+    const int64_t n64 = (T + tc::r64::BR - 1) / tc::r64::BR * ((tc::nkb_padded(D) / 2 + tc::r64::UNIT_ST - 1) / tc::r64::UNIT_ST);
+    const int64_t nunits = std::max(n128, n64);
     return (size_t)std::min<int64_t>(nunits, kSplitMaxPieces) * tc::BN * tc::BM * sizeof(double);
 }
 
@@ -1022,6 +1044,30 @@ static void launch_mode(const CUtensorMap &mK, const CUtensorMap &mKh, const CUt
     (void)cudaLaunchKernelEx(&cfg, tc::attn_tc_kernel<MODE>, mK, mKh, mKq, p);
 }
 
+static void launch_rt64(const CUtensorMap &mK, const CUtensorMap &mKh, const CUtensorMap &mKq, const tc::TcParams &p,
+                        int grid, cudaStream_t s, bool cooperative) {
+    const size_t smem = sizeof(tc::r64::Smem);
+    static std::once_flag once;
+    std::call_once(once, [&] {
+        cudaFuncSetAttribute(tc::r64::rt64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    if (!cooperative) {
+        (void)launch_pdl(tc::r64::rt64_kernel, dim3(grid), dim3(tc::NTHREADS), smem, s, mK, mKh, mKq, p);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(tc::NTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    (void)cudaLaunchKernelEx(&cfg, tc::r64::rt64_kernel, mK, mKh, mKq, p);
+}
+
 // Launch: qsplit (into ws_q) [+ colq] + the persistent tensor-core kernel.
 kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
                           int64_t nq, void *ws_q, void *partials, int *grid_out, float *S, cudaStream_t s,
@@ -1029,15 +1075,18 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
                           float *scales_out, void *ws_pmax) {
     using namespace tc;
     const bool fused_a1 = mode == 2 && scales_out != nullptr && ws_pmax != nullptr;
-    const int64_t nkb = (D + BK - 1) / BK;
-    const int ntiles = (int)((T + BM - 1) / BM);
+    const bool r64 = mode == 2 && use_rt64();  // the fused roundtrip on 64-row tiles (rt64.cuh), opt-in
+    const int trows = r64 ? r64::BR : BM;
+    // r64: K-blocks padded to whole 64-column stages (zero Q tiles and column records past D)
+    const int64_t nkb = r64 ? nkb_padded(D) : (D + BK - 1) / BK;
+    const int ntiles = (int)((T + trows - 1) / trows);
     CUtensorMap mK, mKh, mKq;
-    if (!make_map_f32(&mK, K, T, D)) return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(K) failed");
+    if (!make_map_f32(&mK, K, T, D, trows)) return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(K) failed");
     mKh = mK;
     mKq = mK;
     if (mode == 2) {
-        if (!make_map_f32(&mKh, Kh_out, T, D)) return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(K_hat) failed");
-        if (!make_map(&mKq, Kq_out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, T, D, BK * CODE_KB))
+        if (!make_map_f32(&mKh, Kh_out, T, D, trows)) return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(K_hat) failed");
+        if (!make_map(&mKq, Kq_out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, T, D, BK * CODE_KB, trows))
             return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(Kq) failed");
     } else if (K_hat) {
         if (!make_map_f32(&mKh, K_hat, T, D)) return fail(KVQ_ERR_CUDA, "cuTensorMapEncodeTiled(K_hat) failed");
@@ -1078,7 +1127,7 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
         p.colq = cq;
         p.Kh = Kh_out;
     }
-    p.ngrp = (int)((nkb + CODE_KB - 1) / CODE_KB);
+    p.ngrp = r64 ? (int)((nkb / 2 + r64::UNIT_ST - 1) / r64::UNIT_ST) : (int)((nkb + CODE_KB - 1) / CODE_KB);
     // modes 0/2: whole-tile waves + a split tail when the cost model says so (see make_units, tc_plan_tail);
     // mode 1 (scores): whole tiles
     const int nsm = std::min(device_info().num_sms, kSplitMaxCtas);
@@ -1097,13 +1146,19 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
         launch_mode<0>(mK, mKh, mKq, p, grid, smem, s);
     else if (mode == 1)
         launch_mode<1>(mK, mKh, mKq, p, grid, smem, s);
+    else if (r64)
+        launch_rt64(mK, mKh, mKq, p, grid, s, fused_a1);
     else
         launch_mode<2>(mK, mKh, mKq, p, grid, smem, s, fused_a1);
     if (kvq_status st = check_launch(mode == 0 ? "attn_tc(metrics)" : mode == 1 ? "attn_tc(scores)" : "attn_tc(roundtrip)");
         st != KVQ_OK || !balanced || R == 0)
         return st;
-    (void)launch_pdl(split_combine_kernel, dim3(R, COMBINE_JQ), dim3(BM), 0, s, (const double *)p.split, T, (int)nq,
-                     plan.whole * grid, plan.rt, grid, plan.pieces, reinterpret_cast<Partial *>(partials));
+    if (r64)
+        (void)launch_pdl(r64::split_combine64_kernel, dim3(R, COMBINE_JQ), dim3(r64::BR), 0, s, (const double *)p.split,
+                         T, (int)nq, plan.whole * grid, plan.rt, grid, plan.pieces, reinterpret_cast<Partial *>(partials));
+    else
+        (void)launch_pdl(split_combine_kernel, dim3(R, COMBINE_JQ), dim3(BM), 0, s, (const double *)p.split, T, (int)nq,
+                         plan.whole * grid, plan.rt, grid, plan.pieces, reinterpret_cast<Partial *>(partials));
     return check_launch("attn_tc(split_combine)");
 }
 

@@ -465,6 +465,35 @@ int main(int argc, char **argv) {
             tile_grp<8, G, IL><<<grid, 64, smem>>>(mi, mo, IL == 1 ? mc32 : mc128, ntl, nkb);                 \
         });                                                                                                    \
     }
+    if (getenv("WIDE3")) {  // round 2: the 64-row geometries at the real kernel's 128 KB in flight
+    TILE(8, 32, 128, 1, 3, "tile BR128 BC32  ST8  R4W5", 9);
+    TILE(8, 64, 64, 1, 3, "tile BR64  BC64  ST8  R4W5", 9);
+    TILE(6, 64, 64, 1, 3, "tile BR64  BC64  ST6  R4W5", 9);
+    TILE(16, 32, 64, 1, 3, "tile BR64  BC32  ST16 R4W5", 9);
+    TILE(4, 128, 64, 1, 3, "tile BR64  BC128 ST4  R4W5", 9);
+    TILEW(8, 64, 64, 1, 3, 2, "tile BR64  BC64  ST8 WD2 R4W5", 9);
+    TILE(8, 32, 128, 1, 3, "tile BR128 BC32  ST8  R4W5", 9);
+    TILE(8, 64, 64, 1, 3, "tile BR64  BC64  ST8  R4W5", 9);
+    printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+    return 0;
+    }
+    if (getenv("WIDE2")) {  // round 2: shorter tiles with longer row segments (candidate M = 64 geometries)
+    TILE(4, 32, 128, 1, 3, "tile BR128 BC32  ST4  R4W5", 9);
+    TILE(8, 32, 128, 1, 3, "tile BR128 BC32  ST8  R4W5", 9);
+    TILE(4, 32, 64, 1, 3, "tile BR64  BC32  ST4  R4W5", 9);
+    TILE(8, 32, 64, 1, 3, "tile BR64  BC32  ST8  R4W5", 9);
+    TILE(4, 64, 64, 1, 3, "tile BR64  BC64  ST4  R4W5", 9);
+    TILE(2, 128, 64, 1, 3, "tile BR64  BC128 ST2  R4W5", 9);
+    TILE(3, 128, 64, 1, 3, "tile BR64  BC128 ST3  R4W5", 9);
+    TILE(4, 128, 64, 1, 3, "tile BR64  BC128 ST4  R4W5", 9);
+    TILE(2, 256, 64, 1, 3, "tile BR64  BC256 ST2  R4W5", 9);
+    TILE(4, 128, 32, 1, 3, "tile BR32  BC128 ST4  R4W5", 9);
+    TILE(4, 256, 32, 1, 3, "tile BR32  BC256 ST4  R4W5", 9);
+    TILE(8, 256, 16, 1, 3, "tile BR16  BC256 ST8  R4W5", 9);
+    TILE(4, 256, 16, 1, 3, "tile BR16  BC256 ST4  R4W5", 9);
+    printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+    return 0;
+    }
     if (getenv("WIDE")) {
     TILE(8, 32, 128, 1, 3, "tile BR128 BC32  ST8  R4W5", 9);
     TILE(4, 32, 128, 1, 3, "tile BR128 BC32  ST4  R4W5", 9);

@@ -23,7 +23,7 @@ for tiles in [int(x) for x in os.environ.get("TILES", "16,148").split(",")]:
     for _ in range(3):
         kvq.kvq_roundtrip(K, s, Q)
     torch.cuda.synchronize()
-    buf = np.zeros((64, 16), dtype=np.uint64)
+    buf = np.zeros((64, 48), dtype=np.uint64)
     lib = _lib.load()
     lib.kvq_debug_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
     assert lib.kvq_debug_trace_read(buf.ctypes.data, buf.nbytes) == 0
@@ -41,6 +41,17 @@ for tiles in [int(x) for x in os.environ.get("TILES", "16,148").split(",")]:
     print("  load issue -> full_k seen (0>1):", int(np.median(t[:, 1] - t[:, 0])), " 4 -> MMA sees full_a (9):",
           int(np.median(t[:, 9] - np.maximum(t[:, 4], t[:, 6]))), " MMA 9>10:", int(np.median(t[:, 10] - t[:, 9])),
           " staged(2) -> store sees (7):", int(np.median(t[:, 7] - t[:, 2])), " 7>8:", int(np.median(t[:, 8] - t[:, 7])))
+    w = t[:, 16:24]
+    wl = t[:, 32:40]
+    ok = (w > 0).all(axis=1)
+    spread = (w.max(axis=1) - w.min(axis=1))[ok]
+    lspread = (wl.max(axis=1) - wl.min(axis=1))[ok]
+    print("  staged arrival spread over the team's 8 warps (cycles): median", int(np.median(spread)), " p90",
+          int(np.percentile(spread, 90)), " max", int(spread.max()), "; quantize-done spread: median",
+          int(np.median(lspread)), " p90", int(np.percentile(lspread, 90)), " max", int(lspread.max()))
+    print("  last staged arrival -> store sees (7):", int(np.median((t[:, 7] - w.max(axis=1))[ok])),
+          "; which warp is last (counts):", np.bincount(np.argmax(w[ok], axis=1), minlength=8).tolist())
+    print("  per block spread:", spread[:24].tolist())
     ev = [0, 14, 1, 11, 2, 3, 4, 7, 8, 9, 10]
     print("  absolute (cycles from block 64's load issue); events " + " ".join(f"{e:>6d}" for e in ev))
     for g in range(0, 24):

@@ -45,6 +45,18 @@ def test_fused_step_launch_count(bench, b200, rows, comm, kind, expect):
     assert bench.launches_per_step(args(), comm, kind, rows, 8192) == expect
 
 
+@pytest.mark.parametrize("rows,comm,kind,expect", [
+    (131072, None, None, 5),        # one GPU: colmax, finalize, prep, rt64_kernel, reduce (writes the result)
+    (65536, object(), PEER, 6),     # 2-rank shard: 1024 64-row tiles = 6.9 waves -> whole tiles
+    (32768, object(), PEER, 7),     # 4-rank shard: 512 tiles = 3 waves + 68 tiles in 2 pieces, + split_combine64
+    (16384, object(), PEER, 7),     # 8-rank shard: 256 tiles = 1 wave + 108 tiles in 4 pieces, + split_combine64
+])
+def test_fused_step_launch_count_rt64(bench, b200, monkeypatch, rows, comm, kind, expect):
+    """The opt-in 64-row roundtrip kernel (KVQ_TC_RT64=1, rt64_kernel)."""
+    monkeypatch.setenv("KVQ_TC_RT64", "1")
+    assert bench.launches_per_step(args(), comm, kind, rows, 8192) == expect
+
+
 def test_separate_and_format_launch_counts(bench, b200):
     # scales (2) + quantize + dequantize + metrics (qsplit, attn_tc<0>, reduce)
     assert bench.launches_per_step(args(pipeline="separate"), None, None, 131072, 8192) == 7

@@ -686,3 +686,42 @@ def test_fault_injection_caught_by_hash_compare(kvq, orc, target):
     for name, u in bufs.items():
         if name != target:
             assert sha16(u) == g[keys[name]]
+
+
+# ----------------------------------------------------------------------------- opt-in 64-row roundtrip kernel
+# (KVQ_TC_RT64=1, csrc/rt64.cuh: 64-row tiles, the stage's two 32-column boxes stacked along the MMA's M;
+# parity-green, measured slower than the 128-row kernel: DESIGN §12).
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("T,D,nq", RT_CASES)
+def test_roundtrip_rt64_vs_oracle(kvq, orc, monkeypatch, T, D, nq):
+    monkeypatch.setenv("KVQ_TC_RT64", "1")
+    K = orc.fill(T, D, 6, 1)
+    so, qo, kho = orc.roundtrip(K)
+    Q = orc.fill(nq, D, 43) if nq else None
+    s = kvq.kvq_compute_scales(dev(K))
+    Kq, Kh, out = kvq.kvq_roundtrip(dev(K), s, None if Q is None else dev(Q))
+    m = kvq.metrics_from_device(out)
+    same_bits(host(Kq), qo)
+    same_bits(host(Kh), kho)
+    ss, mx = orc.recon_errors(K, kho)
+    assert m["max_abs"] == mx and (_rel(m["sum_sq"], ss) <= REL or ss == 0)
+    if nq:
+        assert _rel(m["attn_mean_abs"], orc.attention_error(Q, K, kho)) <= REL
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("T,D,nq", SPLIT_CASES)
+def test_roundtrip_rt64_split_tiles_vs_oracle(kvq, orc, monkeypatch, T, D, nq):
+    monkeypatch.setenv("KVQ_TC_RT64", "1")
+    monkeypatch.setenv("KVQ_TC_BALANCE", "1")
+    K = orc.fill(T, D, 7, 1)
+    so, qo, kho = orc.roundtrip(K)
+    Q = orc.fill(nq, D, 43)
+    s = kvq.kvq_compute_scales(dev(K))
+    Kq, Kh, out = kvq.kvq_roundtrip(dev(K), s, dev(Q))
+    m = kvq.metrics_from_device(out)
+    same_bits(host(Kq), qo)
+    same_bits(host(Kh), kho)
+    ss, mx = orc.recon_errors(K, kho)
+    assert m["max_abs"] == mx and _rel(m["sum_sq"], ss) <= REL
+    assert _rel(m["attn_mean_abs"], orc.attention_error(Q, K, kho)) <= REL

@@ -202,3 +202,13 @@ def test_fused_a1_structured(kvq, orc, monkeypatch, name):
     assert np.array_equal(bits(host(q)), bits(qo))
     assert np.array_equal(bits(host(kh)), bits(kho))
     assert kvq.metrics_from_device(out)["max_abs"] == orc.max_abs_error(K, kho)
+
+
+@pytest.mark.parametrize("T,D,nq", [(8192, 1024, 64), (1000, 48, 64), (2047, 4096, 17)])
+def test_fused_a1_path_rt64(kvq, orc, monkeypatch, T, D, nq):
+    """The fused a1 + a2 front end on the opt-in 64-row roundtrip kernel (KVQ_TC_RT64=1)."""
+    monkeypatch.setenv("KVQ_STEP_SMALL", "0")
+    monkeypatch.setenv("KVQ_STEP_FUSED", "1")
+    monkeypatch.setenv("KVQ_TC_RT64", "1")
+    K = orc.fill(T, D, 42, 1)
+    check(kvq, orc, K, orc.fill(nq, D, 43), None, None)
