@@ -285,7 +285,10 @@ def launches_per_step(args, comm, comm_kind, rows, D):
             and rows * D * 4 <= l2 // 2):
         return 3 + combine  # Q split + the tensor-core pass with a1 + a2 fused in front [+ split_combine] + reduce
     if args.format == "int8" and args.pipeline in ("fused", "step"):
-        return scales + 3 + combine + tail
+        if os.environ.get("KVQ_TC_RT64", "0") == "1":
+            return scales + 3 + combine + tail
+        # whole tiles: the pass's last CTA reduces the partials (no reduce_partials launch)
+        return scales + 2 + 2 * combine + tail
     metrics = 3 + combine + tail
     if args.format == "int8":
         return scales + 1 + 1 + metrics  # + quantize + dequantize

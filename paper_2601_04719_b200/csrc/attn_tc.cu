@@ -160,6 +160,13 @@ struct TcParams {
     const float *Kin;    // K for the column-max phase (generic loads)
     float *scales_out;   // [D] s_d = fl32(m_d / 127)
     ColRec *colq_out;    // the per-K-block quantizer records the roundtrip then reads (== colq)
+    // MODE 2 with whole tiles: the CTA that retires last reduces every CTA's partial in a fixed order and writes the
+    // totals (and the metrics when no exchange follows) itself: no reduce_partials launch
+    unsigned *ticket;        // zeroed by prep_kernel; nullptr: reduce_partials_kernel does it
+    const float *scales_in;  // theoretical max = max_d s_d / 2
+    double *sums;            // [4]: sum_sq, attn_abs, n_elems, n_scores (as reduce_partials_kernel)
+    uint64_t *maxes;         // [2]: max_abs, theoretical max (fp64 bit patterns)
+    kvq_metrics *final_out;  // nullable
 };
 
 // Work distribution.  A work unit is one group of CODE_KB K-blocks (one accumulator chunk, one code
@@ -295,9 +302,10 @@ __device__ __forceinline__ void colq_body(const float *__restrict__ scales, int6
 // the column records.
 __global__ void __launch_bounds__(256) prep_kernel(const float *__restrict__ Q, int64_t nq, int64_t D, int64_t nkb,
                                                    uint32_t *__restrict__ qs, const float *__restrict__ scales,
-                                                   ColRec *__restrict__ cq, int nbq) {
+                                                   ColRec *__restrict__ cq, int nbq, unsigned *ticket) {
     pdl_wait();  // Q and the scales of the preceding calls
     pdl_trigger();
+    if (ticket && blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0u;  // the pass's last-CTA ticket
     if ((int)blockIdx.x < nbq)
         qsplit_body(Q, nq, D, nkb, qs, blockIdx.x, nbq);
     else
@@ -417,6 +425,76 @@ __device__ __forceinline__ void fused_scales_phase(const TcParams &p, uint8_t *s
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");  // the records are read by bulk copies (async proxy)
     grid.sync();
+}
+
+// The end of the roundtrip pass with whole tiles (p.ticket set): after its partial is written (thread 0, then a block
+// barrier), every CTA takes a ticket; the last one reduces all G partials in a fixed order with one warp (strided
+// per-lane sums, xor butterfly: deterministic) and writes the totals as reduce_partials_kernel does.  Runs after the
+// warp roles, within the smallest register budget (warpgroup 0's).
+__device__ __forceinline__ void last_cta_reduce(const TcParams &p, int *flag) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, G = gridDim.x;
+    constexpr int NW = NTHREADS / 32;
+    double *sh = reinterpret_cast<double *>(flag + 4);  // [4][NW] (the free input ring)
+    if (tid == 0) {
+        __threadfence();  // this CTA's partial, before its ticket
+        *flag = atomicAdd(p.ticket, 1u) == (unsigned)G - 1;
+    }
+    __syncthreads();
+    if (!*flag) return;  // uniform: the whole CTA reduces (as reduce_partials_kernel, 768 instead of 1024 threads)
+    __threadfence();     // the other CTAs' partials (their tickets came first)
+    double ss = 0.0, at = 0.0, mx = 0.0, th = 0.0;
+    for (int i = tid; i < G; i += NTHREADS) {
+        ss += __ldcg(&p.partials[i].sum_sq);
+        at += __ldcg(&p.partials[i].attn_abs);
+        mx = fmax(mx, __ldcg(&p.partials[i].max_abs));
+    }
+    for (int64_t d = tid; d < p.D; d += NTHREADS) th = fmax(th, (double)__ldcg(p.scales_in + d) / 2.0);
+    for (int o = 16; o > 0; o >>= 1) {
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        at += __shfl_xor_sync(0xffffffffu, at, o);
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        th = fmax(th, __shfl_xor_sync(0xffffffffu, th, o));
+    }
+    if (lane == 0) {
+        sh[wid] = ss;
+        sh[NW + wid] = at;
+        sh[2 * NW + wid] = mx;
+        sh[3 * NW + wid] = th;
+    }
+    __syncthreads();
+    if (wid != 0) return;
+    ss = lane < NW ? sh[lane] : 0.0;
+    at = lane < NW ? sh[NW + lane] : 0.0;
+    mx = lane < NW ? sh[2 * NW + lane] : 0.0;
+    th = lane < NW ? sh[3 * NW + lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        at += __shfl_xor_sync(0xffffffffu, at, o);
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        th = fmax(th, __shfl_xor_sync(0xffffffffu, th, o));
+    }
+    if (lane == 0) {
+        const double n_elems = (double)p.T * (double)p.D, n_scores = (double)p.nq * (double)p.T;
+        const double maxabs = fmax(mx, 0.0);
+        p.sums[0] = ss;
+        p.sums[1] = at;
+        p.sums[2] = n_elems;
+        p.sums[3] = n_scores;
+        p.maxes[0] = (uint64_t)__double_as_longlong(maxabs);
+        p.maxes[1] = (uint64_t)__double_as_longlong(th);
+        if (p.final_out) {
+            kvq_metrics m;
+            m.sum_sq = ss;
+            m.attn_abs_sum = at;
+            m.n_elems = (int64_t)n_elems;
+            m.n_scores = (int64_t)n_scores;
+            m.l2 = sqrt(ss);
+            m.max_abs = maxabs;
+            m.theoretical_max = th;
+            m.attn_mean_abs = n_scores > 0.0 ? at / n_scores : 0.0;
+            *p.final_out = m;
+        }
+    }
 }
 
 // byte address of 16-byte chunk c of row r in a [rows][128 B] tile with the TMA 128B swizzle
@@ -915,6 +993,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc_fence_after();
         tmem_dealloc<TMEM_COLS>(tbase);
     }
+    if constexpr (MODE == 2) {
+        if (p.ticket) last_cta_reduce(p, reinterpret_cast<int *>(s.buf));
+    }
 }
 
 }  // namespace tc
@@ -1072,8 +1153,10 @@ static void launch_rt64(const CUtensorMap &mK, const CUtensorMap &mKh, const CUt
 kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t T, int64_t D, const float *Q,
                           int64_t nq, void *ws_q, void *partials, int *grid_out, float *S, cudaStream_t s,
                           const float *scales, void *ws_colq, int8_t *Kq_out, float *Kh_out, void *ws_split,
-                          float *scales_out, void *ws_pmax) {
+                          float *scales_out, void *ws_pmax, const MetricTotals *fin, unsigned *ticket,
+                          bool *reduced) {
     using namespace tc;
+    if (reduced) *reduced = false;
     const bool fused_a1 = mode == 2 && scales_out != nullptr && ws_pmax != nullptr;
     const bool r64 = mode == 2 && use_rt64();  // the fused roundtrip on 64-row tiles (rt64.cuh), opt-in
     const int trows = r64 ? r64::BR : BM;
@@ -1121,7 +1204,7 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
         } else {
             const unsigned cblocks = (unsigned)std::min<int64_t>((nkb + 7) / 8, 1024);
             (void)launch_pdl(prep_kernel, dim3(qblocks + cblocks), dim3(256), 0, s, Q, nq, D, nkb, qs, scales, cq,
-                             (int)qblocks);
+                             (int)qblocks, ticket);
             if (kvq_status st = check_launch("qsplit+colq"); st != KVQ_OK) return st;
         }
         p.colq = cq;
@@ -1140,6 +1223,15 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
     p.whole = balanced ? plan.whole : 0;
     p.rt = balanced ? plan.rt : 0;
     const int R = balanced ? plan.rt : 0;
+    // whole tiles, separate prep (which zeroes the ticket): the pass reduces its partials itself
+    if (mode == 2 && !r64 && !fused_a1 && !balanced && fin && ticket) {
+        p.ticket = ticket;
+        p.scales_in = scales;
+        p.sums = fin->sums;
+        p.maxes = fin->maxes;
+        p.final_out = fin->fused_out;
+        if (reduced) *reduced = true;
+    }
     const size_t smem = sizeof(Smem);
     if (grid_out) *grid_out = balanced ? grid + COMBINE_JQ * R : grid;  // + one partial per tail tile and quarter
     if (mode == 0)

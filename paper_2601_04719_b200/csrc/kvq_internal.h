@@ -99,7 +99,8 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
                           int64_t nq, void *ws_q, void *partials, int *grid_out, float *S, cudaStream_t s,
                           const float *scales = nullptr, void *ws_colq = nullptr, int8_t *Kq_out = nullptr,
                           float *Kh_out = nullptr, void *ws_split = nullptr, float *scales_out = nullptr,
-                          void *ws_pmax = nullptr);
+                          void *ws_pmax = nullptr, const MetricTotals *fin = nullptr, unsigned *ticket = nullptr,
+                          bool *reduced = nullptr);
 // mode 2 with a1 + a2 fused in front (scales_out, ws_pmax set; cooperative launch): the kvq_step path for an
 // L2-resident K (the pmax workspace holds kSplitMaxCtas x D u32, the largest grid).
 kvq_status launch_roundtrip_fused_a1(const float *K, int64_t T, int64_t D, float *scales_out, int8_t *Kq,

@@ -261,6 +261,7 @@ struct WsLayout {
     void *split;  // tensor-core kernels: fp64 Delta of tiles split between CTAs
     double *sums;
     uint64_t *maxes;
+    unsigned *ticket;  // the roundtrip pass's last-CTA reduction (attn_tc.cu last_cta_reduce)
 };
 
 static WsLayout ws_layout(void *ws, int64_t T, int64_t D) {
@@ -278,6 +279,7 @@ static WsLayout ws_layout(void *ws, int64_t T, int64_t D) {
     off += al256(tc_split_bytes(T, D));
     L.sums = reinterpret_cast<double *>(off);
     L.maxes = reinterpret_cast<uint64_t *>(L.sums + 4);
+    L.ticket = reinterpret_cast<unsigned *>(L.maxes + 2);
     return L;
 }
 
@@ -285,7 +287,7 @@ size_t metrics_workspace_size(int64_t T, int64_t D, int64_t nq) {
     (void)nq;
     const size_t np = (size_t)metrics_partials_count(num_tiles(T));
     return 256 + al256(np * sizeof(Partial)) + al256(tc_qsplit_bytes(D)) + al256(tc_colq_bytes(D)) +
-           al256(tc_split_bytes(T, D)) + 4 * sizeof(double) + 2 * sizeof(uint64_t);
+           al256(tc_split_bytes(T, D)) + 4 * sizeof(double) + 2 * sizeof(uint64_t) + 2 * sizeof(unsigned);
 }
 
 static kvq_status reduce_partials(const WsLayout &L, int64_t nparts, const float *scales, int64_t T, int64_t D,
@@ -358,10 +360,15 @@ kvq_status launch_roundtrip_partials(const float *K, const float *scales, int64_
     if (!force_simt() && tc_roundtrip_eligible(K, Kq, K_hat, T, D, nq)) {
         const WsLayout L = ws_layout(ws, T, D);
         int grid = 0;
+        totals->sums = L.sums;
+        totals->maxes = L.maxes;
+        bool reduced = false;  // whole tiles: the pass's last CTA reduces the partials itself
         if (kvq_status st = launch_attn_tc(2, K, nullptr, T, D, Q, nq, L.qsplit, L.partials, &grid, nullptr, s,
-                                           scales, L.colq, Kq, K_hat, L.split);
+                                           scales, L.colq, Kq, K_hat, L.split, nullptr, nullptr, totals, L.ticket,
+                                           &reduced);
             st != KVQ_OK)
             return st;
+        if (reduced) return KVQ_OK;
         return reduce_partials(L, grid, scales, T, D, nq, totals, s);
     }
     // not eligible for the single pass: fused quantize+dequantize, then the metrics pass

@@ -34,12 +34,12 @@ NCCL = "nccl (libkvq kvq_comm_t)"
 
 
 @pytest.mark.parametrize("rows,comm,kind,expect", [
-    (131072, None, None, 5),        # one GPU: colmax, finalize, prep, attn_tc<2>, reduce (writes the result)
-    (131072, object(), PEER, 6),    # fused colmax+exchange+finalize; + metric exchange + metrics_finalize
-    (131072, object(), NCCL, 6),    # colmax, finalize, prep, attn, reduce, metrics_finalize (NCCL not counted)
-    (65536, object(), PEER, 7),     # 2-rank shard: 512 tiles = 3 waves + 46% -> balanced tail, + split_combine
-    (32768, object(), PEER, 7),     # 4-rank shard: 1.73 waves -> 1 whole wave + 108 tiles in 4 pieces, + split_combine
-    (16384, object(), PEER, 6),     # 8-rank shard: one wave -> whole tiles
+    (131072, None, None, 4),        # one GPU: colmax, finalize, prep, attn_tc<2> (its last CTA reduces the partials)
+    (131072, object(), PEER, 5),    # fused colmax+exchange+finalize; prep, attn; + metric exchange + metrics_finalize
+    (131072, object(), NCCL, 5),    # colmax, finalize, prep, attn, metrics_finalize (NCCL not counted)
+    (65536, object(), PEER, 7),     # 2-rank shard: 512 tiles = 3 waves + 46% -> balanced tail, + split_combine + reduce
+    (32768, object(), PEER, 7),     # 4-rank shard: 1.73 waves -> 1 whole wave + 108 tiles in 4 pieces, + combine + reduce
+    (16384, object(), PEER, 5),     # 8-rank shard: one wave -> whole tiles
 ])
 def test_fused_step_launch_count(bench, b200, rows, comm, kind, expect):
     assert bench.launches_per_step(args(), comm, kind, rows, 8192) == expect
@@ -115,4 +115,4 @@ def test_step_pipeline_launch_counts(bench, b200):
     a = types.SimpleNamespace(format="int8", pipeline="step")
     assert bench.launches_per_step(a, None, None, 1024, 128) == 1        # C1: one cooperative launch
     assert bench.launches_per_step(a, None, None, 8192, 1024) == 4       # C2: qsplit + fused pass + combine + reduce
-    assert bench.launches_per_step(a, None, None, 131072, 8192) == 5     # C4: the two calls
+    assert bench.launches_per_step(a, None, None, 131072, 8192) == 4     # C4: the two calls
