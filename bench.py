@@ -283,7 +283,8 @@ def launches_per_step(args, comm, comm_kind, rows, D):
     l2 = getattr(torch.cuda.get_device_properties(torch.cuda.current_device()), "L2_cache_size", 0)
     if (args.format == "int8" and args.pipeline == "step" and comm is None and D % 16 == 0
             and rows * D * 4 <= l2 // 2):
-        return 3 + combine  # Q split + the tensor-core pass with a1 + a2 fused in front [+ split_combine] + reduce
+        # the tensor-core pass with a1 + a2 and the Q split fused in front [+ split_combine] + reduce
+        return (3 if os.environ.get("KVQ_TC_RT64", "0") == "1" else 2) + combine
     if args.format == "int8" and args.pipeline in ("fused", "step"):
         if os.environ.get("KVQ_TC_RT64", "0") == "1":
             return scales + 3 + combine + tail

@@ -167,6 +167,9 @@ struct TcParams {
     double *sums;            // [4]: sum_sq, attn_abs, n_elems, n_scores (as reduce_partials_kernel)
     uint64_t *maxes;         // [2]: max_abs, theoretical max (fp64 bit patterns)
     kvq_metrics *final_out;  // nullable
+    // MODE 2 with a1 + a2 fused in front: the Q split is done by the column-max phase too (no qsplit launch)
+    const float *Qin;        // Q [nq][D] (nullptr when nq == 0)
+    uint32_t *qsplit_out;    // == qsplit
 };
 
 // Work distribution.  A work unit is one group of CODE_KB K-blocks (one accumulator chunk, one code
@@ -352,6 +355,7 @@ __global__ void __launch_bounds__(BM) split_combine_kernel(const double *__restr
 // grid barrier; Eq. 5/6 for the K-blocks this CTA owns (kb = b, b + G, ...): m_d = max over the partial rows
 // (order-free), s_d = fl32(m_d / 127) (IEEE division), the K-block's quantizer record; grid barrier.  The
 // roundtrip's producer then bulk-loads the records as usual.  `sm` is the (still unused) input ring.
+template <bool QSPLIT = true>  // QSPLIT: also split Q (p.qsplit_out) before the second grid barrier
 __device__ __forceinline__ void fused_scales_phase(const TcParams &p, uint8_t *sm) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -423,7 +427,10 @@ __device__ __forceinline__ void fused_scales_phase(const TcParams &p, uint8_t *s
             if (d < D) p.scales_out[d] = sd;
         }
     }
-    asm volatile("fence.proxy.async.global;" ::: "memory");  // the records are read by bulk copies (async proxy)
+    if constexpr (QSPLIT) {
+        if (p.qsplit_out) qsplit_body(p.Qin, p.nq, D, p.nkb, p.qsplit_out, b, G);  // (the Q split of the step)
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // records and Q tiles are read by bulk copies
     grid.sync();
 }
 
@@ -1176,7 +1183,7 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
     }
     uint32_t *qs = reinterpret_cast<uint32_t *>(ws_q);
     const unsigned qblocks = (unsigned)std::min<int64_t>((nkb * BN * (BK / 4) + 255) / 256, 4096);
-    if (mode != 2 || fused_a1) {  // (fused a1: the tensor-core kernel writes the column records itself)
+    if (mode != 2 || (fused_a1 && r64)) {  // (fused a1: the tensor-core kernel writes the records and Q tiles itself)
         (void)launch_pdl(qsplit_kernel, dim3(qblocks), dim3(256), 0, s, Q, nq, D, nkb, qs);
         if (kvq_status st = check_launch("qsplit"); st != KVQ_OK) return st;
     }
@@ -1201,6 +1208,10 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
             p.Kin = K;
             p.scales_out = scales_out;
             p.colq_out = cq;
+            if (!r64) {
+                p.Qin = Q;
+                p.qsplit_out = qs;
+            }
         } else {
             const unsigned cblocks = (unsigned)std::min<int64_t>((nkb + 7) / 8, 1024);
             (void)launch_pdl(prep_kernel, dim3(qblocks + cblocks), dim3(256), 0, s, Q, nq, D, nkb, qs, scales, cq,

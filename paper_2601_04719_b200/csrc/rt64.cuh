@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t tbase = s.tmem_base;
     pdl_wait();
     pdl_trigger();
-    if (p.pmax) fused_scales_phase(p, s.buf);
+    if (p.pmax) fused_scales_phase<false>(p, s.buf);  // (the Q split stays a launch on this path)
     const Units us = make_units(p);
 
     if (warp < CONV_W0) {

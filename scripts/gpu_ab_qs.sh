@@ -1,0 +1,12 @@
+O=gpurun_out/abq
+mkdir -p $O
+cp ab/libkvq_new.so paper_2601_04719_b200/libkvq.so
+timeout 1500 python -m pytest tests -m gpu -q -x > $O/pytest.txt 2>&1; tail -1 $O/pytest.txt
+: > $O/c2.txt
+for r in 1 2 3; do for v in old new; do cp ab/libkvq_$v.so paper_2601_04719_b200/libkvq.so
+  timeout 120 python bench.py --config C2 --pipeline step --steps 100 --no-e2e --no-cpu > $O/c2.json 2>&1
+  python -c "import json;d=json.loads(open('$O/c2.json').read().strip().splitlines()[-1]);print('$v C2 step round $r', round(d['ms_per_step']*1e3,2), 'b2b', round(d['ms_back_to_back']*1e3,2), 'launches', d['gpu_launches'])" >> $O/c2.txt
+done; done
+cat $O/c2.txt
+VARIANTS="old new" CONFIGS="C4" bash scripts/gpu_ab_bench.sh
+cp ab/libkvq_new.so paper_2601_04719_b200/libkvq.so

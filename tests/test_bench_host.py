@@ -114,5 +114,5 @@ def test_plan_tail_cases(bench):
 def test_step_pipeline_launch_counts(bench, b200):
     a = types.SimpleNamespace(format="int8", pipeline="step")
     assert bench.launches_per_step(a, None, None, 1024, 128) == 1        # C1: one cooperative launch
-    assert bench.launches_per_step(a, None, None, 8192, 1024) == 4       # C2: qsplit + fused pass + combine + reduce
+    assert bench.launches_per_step(a, None, None, 8192, 1024) == 3       # C2: fused pass (Q split inside) + combine + reduce
     assert bench.launches_per_step(a, None, None, 131072, 8192) == 4     # C4: the two calls
