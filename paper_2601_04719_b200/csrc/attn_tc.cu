@@ -400,6 +400,7 @@ __device__ __forceinline__ void fused_scales_phase(const TcParams &p, uint8_t *s
     }
     __syncthreads();
     for (int64_t d = tid; d < D; d += NTHREADS) p.pmax[(int64_t)b * D + d] = smax[d];
+    if (p.ticket && b == 0 && tid == 0) *p.ticket = 0u;  // the pass's last-CTA reduction (no prep launch here)
     grid.sync();
     // the K-blocks this CTA owns: warp w of the 24 folds row groups w, w + 24, ... of column `lane`
     const int lane = tid % 32, wv = tid / 32, nw = NTHREADS / 32;
@@ -1234,8 +1235,8 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
     p.whole = balanced ? plan.whole : 0;
     p.rt = balanced ? plan.rt : 0;
     const int R = balanced ? plan.rt : 0;
-    // whole tiles, separate prep (which zeroes the ticket): the pass reduces its partials itself
-    if (mode == 2 && !r64 && !fused_a1 && !balanced && fin && ticket) {
+    // whole tiles (the ticket zeroed by prep, or by the fused column-max phase): the pass reduces its partials itself
+    if (mode == 2 && !r64 && !balanced && fin && ticket) {
         p.ticket = ticket;
         p.scales_in = scales;
         p.sums = fin->sums;

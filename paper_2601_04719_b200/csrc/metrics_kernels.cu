@@ -344,11 +344,15 @@ kvq_status launch_roundtrip_fused_a1(const float *K, int64_t T, int64_t D, float
     const WsLayout L = ws_layout(ws, T, D);
     const uintptr_t pm = (reinterpret_cast<uintptr_t>(ws) + metrics_workspace_size(T, D, nq) + 255) & ~(uintptr_t)255;
     int grid = 0;
+    totals->sums = L.sums;
+    totals->maxes = L.maxes;
+    bool reduced = false;  // whole tiles: the pass's last CTA reduces the partials itself
     if (kvq_status st = launch_attn_tc(2, K, nullptr, T, D, Q, nq, L.qsplit, L.partials, &grid, nullptr, s,
                                        scales_out, L.colq, Kq, K_hat, L.split, scales_out,
-                                       reinterpret_cast<void *>(pm));
+                                       reinterpret_cast<void *>(pm), totals, L.ticket, &reduced);
         st != KVQ_OK)
         return st;
+    if (reduced) return KVQ_OK;
     return reduce_partials(L, grid, scales_out, T, D, nq, totals, s);
 }
 
