@@ -508,12 +508,49 @@ __device__ __forceinline__ void last_cta_reduce(const TcParams &p, int *flag) {
 // byte address of 16-byte chunk c of row r in a [rows][128 B] tile with the TMA 128B swizzle
 __device__ __forceinline__ uint32_t swz(uint32_t base, int r, int c) { return base + r * 128 + ((c ^ (r & 7)) << 4); }
 
+// The fused converter's rare path for one thread's 16-column row segment (a near-tie quotient, a quotient past
+// the clamp, or an exact-path column) in the FASTCONV variant: re-reads x from the stage, computes every element
+// with the clamp and, where the fast quotient is within 2^-14 of a half-integer (or the column needs it), the IEEE
+// division (quant_exact, the oracle's arithmetic), and writes K_hat in place and the 16 codes to `caddr` itself.
+// The fast path's registers are not touched, so the common path carries no register merges for this branch.
+__device__ __forceinline__ void rare_segment(uint32_t kbase, int r, int h, uint32_t caddr, const ColRec &rec) {
+    uint32_t w[4];
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        const float4 a = lds128(swz(kbase, r, 4 * h + c));
+        const float xs[4] = {a.x, a.y, a.z, a.w};
+        float xh[4], vq[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const int i = 16 * h + 4 * c + e;
+            const float sc = rec.s[i], yy = rec.y[i], xi = xs[e];
+            const float cl = fminf(fmaxf(__fmul_rn(xi, yy), -127.0f), 127.0f);
+            float vv = __fadd_rn(cl, kMagic);
+            const float rr = __fsub_rn(vv, kMagic);
+            float x1 = __fmul_rn(rr, sc);
+            if (fabsf(__fsub_rn(cl, rr)) > kDangerThr || (yy == 0.0f && sc != 0.0f)) {
+                const int cd = quant_exact(xi, sc);
+                vv = __fadd_rn((float)cd, kMagic);
+                x1 = __fmul_rn((float)cd, sc);
+            }
+            xh[e] = x1;
+            vq[e] = vv;
+        }
+        sts128(swz(kbase, r, 4 * h + c), make_float4(xh[0], xh[1], xh[2], xh[3]));
+        w[c] = pack4(vq[0], vq[1], vq[2], vq[3]);
+    }
+    sts128u(caddr, make_uint4(w[0], w[1], w[2], w[3]));
+}
+
 // MODE 0: metrics partials (E = K - K_hat).
 // MODE 1: scores S[i][t] (E = K, or K - K_hat).
 // MODE 2: fused a3+a4+a5+a6: quantize and dequantize the K tile in the
 //         converters (same arithmetic as quant_v4_kernel), write Kq and K_hat,
 //         and contract E = K - K_hat with Q: one HBM pass, 9 bytes/element.
-template <int MODE>
+// FASTCONV (MODE 2 only): the converter variant without register merges on the rare path (253 instead of 325
+// instructions per thread and K-block): faster per CTA, but 2.5% slower where the pass is HBM-bound (C4), so the
+// host uses it only when the pass is bound per CTA (one round of work units: the 8-rank shard, C2).
+template <int MODE, bool FASTCONV = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmKh,
                    const __grid_constant__ CUtensorMap tmKq, const __grid_constant__ TcParams p) {
@@ -767,6 +804,40 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             XH[j] = f2mul(rr, u ? f2pk(s4.z, s4.w) : f2pk(s4.x, s4.y));
                         }
                     }
+                  if constexpr (FASTCONV) {
+                    const bool rare = dmax > kDangerThr || amax > 127.25f || s.cq[sk].any_exact;
+                    if (!code_buf_ready) {
+                        KVQ_WAIT_HOT(&s.cstored[cgrp & 1], ((cgrp >> 1) & 1) ^ 1);
+                        code_buf_ready = true;
+                    }
+                    const uint32_t caddr =
+                        swz(smem_u32(s.buf + 128 * 1024 + (cgrp & 1) * KTILE), r, (kb % CODE_KB) * 2 + h);
+                    if (!rare) {
+#pragma unroll
+                        for (int c = 0; c < 4; c++)
+                            sts128(swz(kbase, r, 4 * h + c), make_float4(f2lo(XH[2 * c]), f2hi(XH[2 * c]),
+                                                                         f2lo(XH[2 * c + 1]), f2hi(XH[2 * c + 1])));
+                        uint4 w;
+                        w.x = pack4(f2lo(V[0]), f2hi(V[0]), f2lo(V[1]), f2hi(V[1]));
+                        w.y = pack4(f2lo(V[2]), f2hi(V[2]), f2lo(V[3]), f2hi(V[3]));
+                        w.z = pack4(f2lo(V[4]), f2hi(V[4]), f2lo(V[5]), f2hi(V[5]));
+                        w.w = pack4(f2lo(V[6]), f2hi(V[6]), f2lo(V[7]), f2hi(V[7]));
+                        sts128u(caddr, w);
+                    } else {
+                        rare_segment(kbase, r, h, caddr, s.cq[sk]);
+                    }
+                    fence_proxy_async();  // generic smem writes -> visible to the TMA (async proxy)
+                    mbar_arrive(&s.staged[sk]);
+                    if (kb == kb1 - 1) cgrp++;
+                    // E from the K_hat the stage now holds (the fast path's or rare_segment's; this thread's own
+                    // stores): no register merge between the two paths
+#pragma unroll
+                    for (int c = 0; c < 4; c++) {
+                        const float4 b = lds128(swz(kbase, r, 4 * h + c));
+                        E[2 * c] = f2sub(X[2 * c], f2pk(b.x, b.y));  // exact (fact 4)
+                        E[2 * c + 1] = f2sub(X[2 * c + 1], f2pk(b.z, b.w));
+                    }
+                  } else {
 #ifdef KVQ_EXP_NODANGER  // timing experiments only (near-tie quotients not repaired: codes may differ)
                     if (s.cq[sk].any_exact) {
 #else
@@ -826,6 +897,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     if (kb == kb1 - 1) cgrp++;
 #pragma unroll
                     for (int j = 0; j < 8; j++) E[j] = f2sub(X[j], XH[j]);  // exact (fact 4)
+                  }
                 }
                 if (MODE != 1) {
                     // e^2 summed over the 16 columns in fp32 (two interleaved partial sums), blocks carried in fp64
@@ -1108,15 +1180,15 @@ TailPlan tc_plan_tail(int ntiles, int ngrp, int nsm, int force) {
     return whole;
 }
 
-template <int MODE>
+template <int MODE, bool FASTCONV = false>
 static void launch_mode(const CUtensorMap &mK, const CUtensorMap &mKh, const CUtensorMap &mKq, const tc::TcParams &p,
                         int grid, size_t smem, cudaStream_t s, bool cooperative = false) {
     static std::once_flag once;
     std::call_once(once, [&] {
-        cudaFuncSetAttribute(tc::attn_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(tc::attn_tc_kernel<MODE, FASTCONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     });
     if (!cooperative) {
-        (void)launch_pdl(tc::attn_tc_kernel<MODE>, dim3(grid), dim3(tc::NTHREADS), smem, s, mK, mKh, mKq, p);
+        (void)launch_pdl(tc::attn_tc_kernel<MODE, FASTCONV>, dim3(grid), dim3(tc::NTHREADS), smem, s, mK, mKh, mKq, p);
         return;
     }
     // grid barriers inside (fused a1 + a2): a cooperative launch guarantees co-residency (1 CTA per SM)
@@ -1130,7 +1202,7 @@ static void launch_mode(const CUtensorMap &mK, const CUtensorMap &mKh, const CUt
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    (void)cudaLaunchKernelEx(&cfg, tc::attn_tc_kernel<MODE>, mK, mKh, mKq, p);
+    (void)cudaLaunchKernelEx(&cfg, tc::attn_tc_kernel<MODE, FASTCONV>, mK, mKh, mKq, p);
 }
 
 static void launch_rt64(const CUtensorMap &mK, const CUtensorMap &mKh, const CUtensorMap &mKq, const tc::TcParams &p,
@@ -1245,6 +1317,10 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
         if (reduced) *reduced = true;
     }
     const size_t smem = sizeof(Smem);
+    // the pass is bound per CTA when every CTA gets at most one round of work (whole tiles in one wave, or a split
+    // plan with no whole-tile wave): take the faster converter there (KVQ_TC_FASTCONV=0|1 forces it off / on)
+    bool fastconv = balanced ? plan.whole == 0 : ntiles <= grid;
+    if (const char *e = std::getenv("KVQ_TC_FASTCONV")) fastconv = e[0] == '1';
     if (grid_out) *grid_out = balanced ? grid + COMBINE_JQ * R : grid;  // + one partial per tail tile and quarter
     if (mode == 0)
         launch_mode<0>(mK, mKh, mKq, p, grid, smem, s);
@@ -1252,6 +1328,8 @@ kvq_status launch_attn_tc(int mode, const float *K, const float *K_hat, int64_t 
         launch_mode<1>(mK, mKh, mKq, p, grid, smem, s);
     else if (r64)
         launch_rt64(mK, mKh, mKq, p, grid, s, fused_a1);
+    else if (fastconv)
+        launch_mode<2, true>(mK, mKh, mKq, p, grid, smem, s, fused_a1);
     else
         launch_mode<2>(mK, mKh, mKq, p, grid, smem, s, fused_a1);
     if (kvq_status st = check_launch(mode == 0 ? "attn_tc(metrics)" : mode == 1 ? "attn_tc(scores)" : "attn_tc(roundtrip)");

@@ -725,3 +725,43 @@ def test_roundtrip_rt64_split_tiles_vs_oracle(kvq, orc, monkeypatch, T, D, nq):
     ss, mx = orc.recon_errors(K, kho)
     assert m["max_abs"] == mx and _rel(m["sum_sq"], ss) <= REL
     assert _rel(m["attn_mean_abs"], orc.attention_error(Q, K, kho)) <= REL
+
+
+# The two converter variants of the fused pass (attn_tc.cu FASTCONV: taken automatically when every CTA gets one
+# round of work units, e.g. the shapes above; the other one for multi-wave passes such as C4): both forced on shapes
+# with near-ties, clamped quotients (caller scales below max/127) and exact-path columns.
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("fast", ["0", "1"])
+@pytest.mark.parametrize("T,D,nq", [(1000, 1024, 64), (300, 128, 17), (19100, 1024, 33)])
+def test_roundtrip_converter_variants(kvq, orc, monkeypatch, fast, T, D, nq):
+    monkeypatch.setenv("KVQ_TC_FASTCONV", fast)
+    K = orc.fill(T, D, 9, 1)
+    so, qo, kho = orc.roundtrip(K)
+    Q = orc.fill(nq, D, 43)
+    s = kvq.kvq_compute_scales(dev(K))
+    Kq, Kh, out = kvq.kvq_roundtrip(dev(K), s, dev(Q))
+    m = kvq.metrics_from_device(out)
+    same_bits(host(Kq), qo)
+    same_bits(host(Kh), kho)
+    ss, mx = orc.recon_errors(K, kho)
+    assert m["max_abs"] == mx and _rel(m["sum_sq"], ss) <= REL
+    assert _rel(m["attn_mean_abs"], orc.attention_error(Q, K, kho)) <= REL
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("fast", ["0", "1"])
+def test_roundtrip_converter_variants_given_scales(kvq, orc, monkeypatch, fast):
+    """Caller scales below max/127 (clamped codes), a subnormal-scale column and a zero column, both variants."""
+    monkeypatch.setenv("KVQ_TC_FASTCONV", fast)
+    T, D, nq = 700, 256, 64
+    K = orc.fill(T, D, 10, 1)
+    K[:, 5] = 0.0
+    K[:, 9] *= np.float32(2.0 ** -140)
+    so, _, _ = orc.roundtrip(K)
+    s = (so * np.float32(0.75)).astype(np.float32)  # quotients past +-127: the clamp decides
+    qo = orc.quantize(K, s)
+    kho = orc.dequantize(qo, s)
+    Q = orc.fill(nq, D, 43)
+    Kq, Kh, out = kvq.kvq_roundtrip(dev(K), dev(s), dev(Q))
+    same_bits(host(Kq), qo)
+    same_bits(host(Kh), kho)
