@@ -279,8 +279,10 @@ kvq_status kvq_error_metrics(const float *K, const float *K_hat, int64_t T, int6
  * Single pass when 1 <= nq <= 64, D % 16 == 0 and K, Kq, K_hat are 16-byte
  * aligned; otherwise the same results from the separate kernels.
  * scales: [D] from kvq_compute_scales.  out_dev: DEVICE kvq_metrics, async.
- * workspace: kvq_roundtrip_workspace_size(T, D, nq) bytes.  comm as in
- * kvq_error_metrics_async. */
+ * workspace: kvq_roundtrip_workspace_size(T, D, nq) bytes [device], not shared by
+ * calls in flight at the same time (it holds the per-CTA partials and the ticket
+ * with which the pass's last CTA reduces them when its tiles are whole).  comm as
+ * in kvq_error_metrics_async. */
 size_t kvq_roundtrip_workspace_size(int64_t T, int64_t D, int64_t nq);
 kvq_status kvq_roundtrip(const float *K, const float *scales, int64_t T, int64_t D, int8_t *Kq,
                          float *K_hat, const float *Q, int64_t nq, void *workspace,
