@@ -471,7 +471,10 @@ StreamPlan plan_stream(int64_t rows, int64_t cols, int threads_per_sm) {
     return p;
 }
 
-constexpr int kUColmax = 8, kUQuant = 4, kUDequant = 8;
+#ifndef KVQ_UQUANT
+#define KVQ_UQUANT 8  // loads in flight per thread of the quantize-alone kernel (C4: 8 -> 0.848 ms, 4 -> 0.863-0.868, 2 -> 0.864-0.877)
+#endif
+constexpr int kUColmax = 8, kUQuant = KVQ_UQUANT, kUDequant = 8;
 
 // Row-slab kernels: scales read as float4 (16-byte aligned), grid.x < 2^31, cols4 < 2^31.
 static bool slab_ok(int64_t cols4, const float *scales) {
@@ -536,6 +539,11 @@ kvq_status launch_quantize(const float *K, const float *scales, int64_t T, int64
         if (K_hat && slab_ok(cols4, scales) && slab_blocks(sg) < (1LL << 31)) {
             quant_slab_kernel<true><<<(unsigned)slab_blocks(sg), kThreads, 0, s>>>(
                 K4, reinterpret_cast<const float4 *>(scales), Q4, H4, sg);
+#ifdef KVQ_QSLAB  // experiments: quantize alone on the row-slab grid
+        } else if (!K_hat && slab_ok(cols4, scales) && slab_blocks(sg) < (1LL << 31)) {
+            quant_slab_kernel<false><<<(unsigned)slab_blocks(sg), kThreads, 0, s>>>(
+                K4, reinterpret_cast<const float4 *>(scales), Q4, nullptr, sg);
+#endif
         } else if (K_hat) {
             StreamPlan p = plan_stream(T, cols4, KVQ_RESIDENT((quant_v4_kernel<kUQuant, true, 1>), 0));
             quant_v4_kernel<kUQuant, true, 1><<<p.blocks, kThreads, 0, s>>>(K4, scales, Q4, H4, n / 4, cols4, p.G);
