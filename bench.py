@@ -157,6 +157,35 @@ def oracle_step(cfg, rows: int):
     return t, rows * D
 
 
+def oracle_step_all_cores(cfg, rows: int, cores: int):
+    """SURVEY §8(d)'s optional all-cores CPU line: the same oracle functions (unchanged, single-threaded C) on
+    `cores` row blocks of the same sample, one thread each (ctypes releases the GIL), wall clock per pass; the
+    column maxima of the blocks are combined with an exact max before Eq. 5/6.  L2/max and attention are not
+    timed here.  Returns ({pass: seconds}, elements)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    import oracle
+    D = cfg["D"]
+    K = oracle.fill(rows, D, oracle.SEED_K)
+    blocks = [b for b in np.array_split(K, cores) if b.shape[0]]
+    blocks = [np.ascontiguousarray(b) for b in blocks]
+    t = {}
+    with ThreadPoolExecutor(max_workers=len(blocks)) as ex:
+        t0 = time.perf_counter()
+        maxes = [np.zeros(D, np.float32) for _ in blocks]
+        list(ex.map(oracle.absmax_rows, blocks, maxes))
+        s = oracle.scales_from_absmax(np.maximum.reduce(maxes))
+        t1 = time.perf_counter()
+        qs = list(ex.map(lambda b: oracle.quantize(b, s), blocks))
+        t2 = time.perf_counter()
+        list(ex.map(lambda q: oracle.dequantize(q, s), qs))
+        t3 = time.perf_counter()
+    t = {"scales": t1 - t0, "quantize": t2 - t1, "dequantize": t3 - t2}
+    return t, rows * D
+
+
 def qdq_seconds(t: dict) -> float:
     """The metric's own mix (quantize+dequantize elements/s): scales + quantize + dequantize."""
     return t["scales"] + t["quantize"] + t["dequantize"]
@@ -599,6 +628,14 @@ def run_kvq(args, cfg, rank, world, local_rank):
                          f"scales, quantize, dequantize, L2/max, attention (nq={nq}); plain C single thread "
                          f"pinned to one core, generation excluded",
                "seconds": sum(t_cpu.values()), **host_info()}
+        ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+        if ncores > 1:
+            t_all, n_all = oracle_step_all_cores(cfg, rows_cpu, ncores)
+            cpu["all_cores"] = {"value": n_all / qdq_seconds(t_all), "unit": "elements/s", "cores": ncores,
+                                "per_pass_s": t_all,
+                                "method": "the same oracle functions on row blocks, one thread per core (ctypes "
+                                          "releases the GIL); block column maxima combined with an exact max; "
+                                          "scales+quantize+dequantize, same sample"}
     line = {
         "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "ms_min": min(per_step), "ms_mean": statistics.mean(per_step),

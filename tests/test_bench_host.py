@@ -116,3 +116,21 @@ def test_step_pipeline_launch_counts(bench, b200):
     assert bench.launches_per_step(a, None, None, 1024, 128) == 1        # C1: one cooperative launch
     assert bench.launches_per_step(a, None, None, 8192, 1024) == 3       # C2: fused pass (Q split inside) + combine + reduce
     assert bench.launches_per_step(a, None, None, 131072, 8192) == 4     # C4: the two calls
+
+
+def test_all_cores_oracle_line(bench):
+    """SURVEY §8(d)'s optional all-cores CPU line: the unchanged oracle functions on row blocks in threads; the
+    combined column maxima give bit-identical scales to the one-core oracle."""
+    import numpy as np
+
+    import oracle
+    cfg = {"D": 256, "nq": 8, "T": 1000, "name": "t"}
+    t, n = bench.oracle_step_all_cores(cfg, 300, 4)
+    assert n == 300 * 256 and set(t) == {"scales", "quantize", "dequantize"} and all(v >= 0 for v in t.values())
+    K = oracle.fill(300, 256, oracle.SEED_K)
+    blocks = [np.ascontiguousarray(b) for b in np.array_split(K, 4)]
+    maxes = [np.zeros(256, np.float32) for _ in blocks]
+    for b, m in zip(blocks, maxes):
+        oracle.absmax_rows(b, m)
+    s = oracle.scales_from_absmax(np.maximum.reduce(maxes))
+    assert np.array_equal(s.view(np.uint32), oracle.compute_scales(K).view(np.uint32))
