@@ -159,9 +159,10 @@ def oracle_step(cfg, rows: int):
 
 def oracle_step_all_cores(cfg, rows: int, cores: int):
     """SURVEY §8(d)'s optional all-cores CPU line: the same oracle functions (unchanged, single-threaded C) on
-    `cores` row blocks of the same sample, one thread each (ctypes releases the GIL), wall clock per pass; the
-    column maxima of the blocks are combined with an exact max before Eq. 5/6.  L2/max and attention are not
-    timed here.  Returns ({pass: seconds}, elements)."""
+    `cores` row blocks of the same sample, one thread each (ctypes releases the GIL), wall clock per pass.  The
+    scales are Alg. 1 (compute_scales, as in the one-core line) per block, combined with an exact max: fl32(m/127)
+    is monotonic in m, so the max of the blocks' scales is the scale of the global column max.  L2/max and
+    attention are not timed here.  Returns ({pass: seconds}, elements)."""
     from concurrent.futures import ThreadPoolExecutor
 
     import numpy as np
@@ -174,9 +175,7 @@ def oracle_step_all_cores(cfg, rows: int, cores: int):
     t = {}
     with ThreadPoolExecutor(max_workers=len(blocks)) as ex:
         t0 = time.perf_counter()
-        maxes = [np.zeros(D, np.float32) for _ in blocks]
-        list(ex.map(oracle.absmax_rows, blocks, maxes))
-        s = oracle.scales_from_absmax(np.maximum.reduce(maxes))
+        s = np.maximum.reduce(list(ex.map(oracle.compute_scales, blocks)))
         t1 = time.perf_counter()
         qs = list(ex.map(lambda b: oracle.quantize(b, s), blocks))
         t2 = time.perf_counter()
@@ -634,8 +633,8 @@ def run_kvq(args, cfg, rank, world, local_rank):
             cpu["all_cores"] = {"value": n_all / qdq_seconds(t_all), "unit": "elements/s", "cores": ncores,
                                 "per_pass_s": t_all,
                                 "method": "the same oracle functions on row blocks, one thread per core (ctypes "
-                                          "releases the GIL); block column maxima combined with an exact max; "
-                                          "scales+quantize+dequantize, same sample"}
+                                          "releases the GIL); the blocks' Alg. 1 scales combined with an exact "
+                                          "max; scales+quantize+dequantize, same sample"}
     line = {
         "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "ms_min": min(per_step), "ms_mean": statistics.mean(per_step),

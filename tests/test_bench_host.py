@@ -127,10 +127,8 @@ def test_all_cores_oracle_line(bench):
     cfg = {"D": 256, "nq": 8, "T": 1000, "name": "t"}
     t, n = bench.oracle_step_all_cores(cfg, 300, 4)
     assert n == 300 * 256 and set(t) == {"scales", "quantize", "dequantize"} and all(v >= 0 for v in t.values())
-    K = oracle.fill(300, 256, oracle.SEED_K)
-    blocks = [np.ascontiguousarray(b) for b in np.array_split(K, 4)]
-    maxes = [np.zeros(256, np.float32) for _ in blocks]
-    for b, m in zip(blocks, maxes):
-        oracle.absmax_rows(b, m)
-    s = oracle.scales_from_absmax(np.maximum.reduce(maxes))
-    assert np.array_equal(s.view(np.uint32), oracle.compute_scales(K).view(np.uint32))
+    for dist in (0, 1):  # uniform and outlier-channel keys
+        K = oracle.fill(300, 256, oracle.SEED_K, dist)
+        blocks = [np.ascontiguousarray(b) for b in np.array_split(K, 4)]
+        s = np.maximum.reduce([oracle.compute_scales(b) for b in blocks])  # fl32(m/127) is monotonic in m
+        assert np.array_equal(s.view(np.uint32), oracle.compute_scales(K).view(np.uint32))
