@@ -765,3 +765,65 @@ def test_roundtrip_converter_variants_given_scales(kvq, orc, monkeypatch, fast):
     Kq, Kh, out = kvq.kvq_roundtrip(dev(K), dev(s), dev(Q))
     same_bits(host(Kq), qo)
     same_bits(host(Kh), kho)
+
+
+# ----------------------------------------------------------------------------- past 2^31 elements
+@pytest.mark.timeout(1200)
+def test_step_past_2pow31_elements(kvq, orc):
+    """Maximum sizes: T * D = 2,147,786,752 > 2^31 elements (8.6 GB of keys; no 32-bit element index may wrap):
+    kvq_compute_scales + kvq_roundtrip (bench.py's step) vs the oracle streaming the same rows on the CPU -- scales bit
+    for bit (Alg. 1 over all rows, in row blocks), codes and K_hat bit for bit on rows at the start, across the
+    2^31-element boundary and at the ragged end, max-abs exact against those rows' bound."""
+    T, D, nq = (1 << 18) + 37, 8192, 64
+    assert T * D > (1 << 31)
+    Kd = kvq.kvq_synth_fill(T, D, seed=42)
+    Qd = kvq.kvq_synth_fill(nq, D, seed=43)
+    s = torch.empty(D, dtype=torch.float32, device="cuda")
+    Kq = torch.empty(T, D, dtype=torch.int8, device="cuda")
+    Kh = torch.empty(T, D, dtype=torch.float32, device="cuda")
+    ws = torch.empty(kvq.kvq_roundtrip_workspace_size(T, D, nq), dtype=torch.uint8, device="cuda")
+    mout = torch.empty(kvq.METRICS_BYTES, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+    kvq.kvq_compute_scales(Kd, s, stream=st)
+    kvq.kvq_roundtrip(Kd, s, Qd, Kq, Kh, out_dev=mout, workspace=ws, stream=st)
+    m = kvq.metrics_from_device(mout)
+    # the oracle's column maxima over all rows, streamed in row blocks (generation included)
+    mx = np.zeros(D, np.float32)
+    for r0 in range(0, T, 16384):
+        orc.absmax_rows(orc.fill(min(16384, T - r0), D, 42, 0, r0), mx)
+    so = orc.scales_from_absmax(mx)
+    same_bits(host(s), so)
+    edge = (1 << 31) // D  # the row holding element 2^31
+    for r0 in (0, edge - 20, T - 40):  # (edge + 20 <= T)
+        Kr = orc.fill(40, D, 42, 0, r0)
+        qo = orc.quantize(Kr, so)
+        same_bits(host(Kq[r0:r0 + 40]), qo)
+        same_bits(host(Kh[r0:r0 + 40]), orc.dequantize(qo, so))
+    assert m["n_elems"] == T * D and m["n_scores"] == nq * T
+    assert 0.0 < m["max_abs"] <= m["theoretical_max"] * (1 + 2.0 ** -15)
+    assert np.isfinite(m["attn_mean_abs"]) and 0.05 < m["attn_mean_abs"] < 0.2  # ~0.095 at D = 8192 (P:481)
+
+
+@pytest.mark.timeout(1200)
+def test_separate_calls_past_2pow31_elements(kvq, orc):
+    """The paper's separate calls (kvq_quantize, kvq_dequantize, kvq_error_metrics) and kvq_quantize_fused at
+    T * D > 2^31: codes and K_hat identical to the single-pass roundtrip's on every row (device compare), metrics
+    equal within 1e-5."""
+    T, D, nq = (1 << 18) + 37, 8192, 64
+    Kd = kvq.kvq_synth_fill(T, D, seed=42)
+    Qd = kvq.kvq_synth_fill(nq, D, seed=43)
+    s = kvq.kvq_compute_scales(Kd)
+    Kq, Kh, out = kvq.kvq_roundtrip(Kd, s, Qd)
+    m = kvq.metrics_from_device(out)
+    q2 = kvq.kvq_quantize(Kd, s)
+    assert torch.equal(q2, Kq)
+    del q2
+    h2 = kvq.kvq_dequantize(Kq, s)
+    assert torch.equal(h2.view(torch.int32), Kh.view(torch.int32))
+    m2 = kvq.kvq_error_metrics(Kd, h2, Qd, s)
+    assert m2["max_abs"] == m["max_abs"] and _rel(m2["l2"], m["l2"]) <= REL
+    assert _rel(m2["attn_mean_abs"], m["attn_mean_abs"]) <= REL
+    del h2
+    s3, q3, h3, _ = kvq.kvq_quantize_fused(Kd)
+    assert torch.equal(s3.view(torch.int32), s.view(torch.int32)) and torch.equal(q3, Kq)
+    assert torch.equal(h3.view(torch.int32), Kh.view(torch.int32))
