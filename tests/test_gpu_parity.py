@@ -827,3 +827,40 @@ def test_separate_calls_past_2pow31_elements(kvq, orc):
     s3, q3, h3, _ = kvq.kvq_quantize_fused(Kd)
     assert torch.equal(s3.view(torch.int32), s.view(torch.int32)) and torch.equal(q3, Kq)
     assert torch.equal(h3.view(torch.int32), Kh.view(torch.int32))
+
+
+@pytest.mark.timeout(1200)
+def test_formats_past_2pow31_elements(kvq, orc):
+    """FP8 E4M3 and INT4 packed (NEXT-1, NEXT-3) at T * D > 2^31: scales bit-exact against the oracle's (from the
+    column maxima streamed over all rows), codes / packed bytes / K_hat bit-exact on rows around the 2^31-element
+    row and at the ragged end."""
+    T, D = (1 << 18) + 37, 8192
+    Kd = kvq.kvq_synth_fill(T, D, seed=42)
+    mx = np.zeros(D, np.float32)
+    for r0 in range(0, T, 16384):
+        orc.absmax_rows(orc.fill(min(16384, T - r0), D, 42, 0, r0), mx)
+    L = orc.lib()
+    edge = (1 << 31) // D
+    # E4M3
+    s8 = kvq.kvq_compute_scales_fmt(Kd, kvq.FMT_E4M3)
+    so8 = np.empty(D, np.float32)
+    L.kvqo_scales_from_absmax_e4m3(orc._p(mx), D, orc._p(so8))
+    same_bits(host(s8), so8)
+    q8, h8 = kvq.kvq_quantize_e4m3(Kd, s8, want_khat=True)
+    for r0 in (edge - 20, T - 40):
+        Kr = orc.fill(40, D, 42, 0, r0)
+        qo = orc.quantize_e4m3(Kr, so8)
+        same_bits(host(q8[r0:r0 + 40]), qo)
+        same_bits(host(h8[r0:r0 + 40]), orc.dequantize_e4m3(qo, so8))
+    del q8, h8
+    # INT4 packed
+    s4 = kvq.kvq_compute_scales_fmt(Kd, kvq.FMT_INT4)
+    so4 = np.empty(D, np.float32)
+    L.kvqo_scales_from_absmax_q(orc._p(mx), D, orc.QMAX[4], orc._p(so4))
+    same_bits(host(s4), so4)
+    p4, h4 = kvq.kvq_quantize_packed(Kd, s4, 4, want_khat=True)
+    for r0 in (edge - 20, T - 40):
+        Kr = orc.fill(40, D, 42, 0, r0)
+        qo = orc.quantize_q(Kr, so4, 4)
+        same_bits(host(p4[r0:r0 + 40]), orc.pack_codes(qo, 4))
+        same_bits(host(h4[r0:r0 + 40]), orc.dequantize(qo, so4))
