@@ -113,3 +113,27 @@ def test_scores_from_codes_nonfinite_query_rows(kvq, orc):
     ref_ok = orc.scores(Q[good], Kh)
     cond = np.abs(Q[good].astype(np.float64)) @ np.abs(Kh.astype(np.float64)).T
     assert float((np.abs(S[good] - ref_ok) / cond).max()) <= REL
+
+
+@pytest.mark.timeout(1200)
+def test_scores_from_codes_past_2pow31_elements(kvq, orc):
+    """T * D > 2^31 code elements: scores straight from the codes against the oracle's fp64 Q . K_hat^T on rows
+    around the 2^31-element row and at the ragged end (the oracle's K_hat from the GPU's scales, which the int8
+    tests pin bit for bit against the oracle at this size)."""
+    T, D, nq = (1 << 18) + 37, 8192, 64
+    Kd = kvq.kvq_synth_fill(T, D, seed=42)
+    Qd = kvq.kvq_synth_fill(nq, D, seed=43)
+    s = kvq.kvq_compute_scales(Kd)
+    q = kvq.kvq_quantize(Kd, s)
+    del Kd
+    S = kvq.kvq_scores_from_codes(Qd, q, s)
+    torch.cuda.synchronize()
+    sh = s.cpu().numpy()
+    Q = orc.fill(nq, D, 43)
+    edge = (1 << 31) // D
+    for r0 in (edge - 20, T - 40):
+        Kh = orc.dequantize(orc.quantize(orc.fill(40, D, 42, 0, r0), sh), sh)
+        ref = orc.scores(Q, Kh)
+        cond = np.abs(Q.astype(np.float64)) @ np.abs(Kh.astype(np.float64)).T
+        got = S[:, r0:r0 + 40].cpu().numpy()
+        assert (np.abs(got - ref) / np.maximum(cond, 1e-300)).max() <= REL
