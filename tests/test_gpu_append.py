@@ -117,3 +117,31 @@ def test_append_errors(kvq):
     with pytest.raises(kvq.KvqError):  # scales aliasing K
         check(kvq.load().kvq_append(K.data_ptr(), 0, 1, 8, st.data_ptr(), K.data_ptr(), q.data_ptr(), None,
                                     ws.data_ptr(), ws.numel(), None, None), "x")
+
+
+@pytest.mark.timeout(1200)
+def test_append_past_2pow31_elements(kvq, orc):
+    """A cache past 2^31 key elements: a prefill of T0 rows (T0 * D > 2^31), then a decode append whose row
+    doubles a few columns' maxima, so those columns are re-quantized over every old row (element indices past
+    2^31).  Scales and the sampled rows' codes / K_hat equal the oracle's batch method on the whole prefix."""
+    D = 8192
+    T0 = (1 << 18) + 36
+    cache = kvq.AppendCache(T0 + 1, D)
+    cache.append(kvq.kvq_synth_fill(T0, D, seed=42))
+    row = orc.fill(1, D, 42, 0, T0)
+    grown = [3, 1000, 8191]
+    row[0, grown] = np.float32(3.0)  # |K| < 1 elsewhere: these three scales grow
+    cache.append(torch.from_numpy(row).cuda())
+    assert cache.T == T0 + 1 and cache.T * D > (1 << 31)
+    mx = np.zeros(D, np.float32)
+    for r0 in range(0, T0, 16384):
+        orc.absmax_rows(orc.fill(min(16384, T0 - r0), D, 42, 0, r0), mx)
+    orc.absmax_rows(row, mx)
+    so = orc.scales_from_absmax(mx)
+    same_bits(host(cache.scales), so, "scales")
+    edge = (1 << 31) // D
+    for r0 in (0, edge - 20, T0 - 39):
+        Kr = orc.fill(40, D, 42, 0, r0) if r0 + 40 <= T0 else np.concatenate([orc.fill(T0 - r0, D, 42, 0, r0), row])
+        qo = orc.quantize(Kr, so)
+        same_bits(host(cache.Kq[r0:r0 + 40]), qo, f"codes {r0}")
+        same_bits(host(cache.K_hat[r0:r0 + 40]), orc.dequantize(qo, so), f"K_hat {r0}")
