@@ -44,7 +44,6 @@ static kvq_status cuda_check(cudaError_t e, const char *what) {
 __global__ void probe_kernel() {}
 
 namespace {
-constexpr int kMaxDevices = 64;
 std::mutex g_mu;
 int g_state[kMaxDevices];  // 0 unknown, 1 ok, 2 unsupported
 DeviceInfo g_info[kMaxDevices];

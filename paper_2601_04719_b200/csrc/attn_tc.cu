@@ -1183,10 +1183,7 @@ TailPlan tc_plan_tail(int ntiles, int ngrp, int nsm, int force) {
 template <int MODE, bool FASTCONV = false>
 static void launch_mode(const CUtensorMap &mK, const CUtensorMap &mKh, const CUtensorMap &mKq, const tc::TcParams &p,
                         int grid, size_t smem, cudaStream_t s, bool cooperative = false) {
-    static std::once_flag once;
-    std::call_once(once, [&] {
-        cudaFuncSetAttribute(tc::attn_tc_kernel<MODE, FASTCONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    });
+    ensure_max_smem<tc::attn_tc_kernel<MODE, FASTCONV>>((int)smem);
     if (!cooperative) {
         (void)launch_pdl(tc::attn_tc_kernel<MODE, FASTCONV>, dim3(grid), dim3(tc::NTHREADS), smem, s, mK, mKh, mKq, p);
         return;
@@ -1208,10 +1205,7 @@ static void launch_mode(const CUtensorMap &mK, const CUtensorMap &mKh, const CUt
 static void launch_rt64(const CUtensorMap &mK, const CUtensorMap &mKh, const CUtensorMap &mKq, const tc::TcParams &p,
                         int grid, cudaStream_t s, bool cooperative) {
     const size_t smem = sizeof(tc::r64::Smem);
-    static std::once_flag once;
-    std::call_once(once, [&] {
-        cudaFuncSetAttribute(tc::r64::rt64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    });
+    ensure_max_smem<tc::r64::rt64_kernel>((int)smem);
     if (!cooperative) {
         (void)launch_pdl(tc::r64::rt64_kernel, dim3(grid), dim3(tc::NTHREADS), smem, s, mK, mKh, mKq, p);
         return;

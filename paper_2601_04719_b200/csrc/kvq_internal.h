@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <utility>
 
@@ -189,6 +190,21 @@ cudaError_t launch_pdl(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t sme
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
+}
+
+// The dynamic shared-memory opt-in of a kernel, once per device (cudaFuncSetAttribute acts on the current
+// device, so a process driving several GPUs needs it on each).  One set of flags per kernel (K is the kernel).
+constexpr int kMaxDevices = 64;
+template <auto K>
+inline void ensure_max_smem(int bytes) {
+    static std::once_flag flags[kMaxDevices];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+        cudaGetLastError();
+        (void)cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        return;
+    }
+    std::call_once(flags[dev], [&] { (void)cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); });
 }
 
 }  // namespace kvq

@@ -381,10 +381,7 @@ kvq_status launch_scores_codes(const float *Q, int64_t nq, const int8_t *Kq, con
     }
     ScParams p{f, bad, Q, scales, Kq, S, T, D, (int)nq, (int)((T + BM - 1) / BM), (int)nkb};
     const int grid = 2 * std::min(p.ntiles, device_info().num_sms / 2);
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(scores_codes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
-    });
+    ensure_max_smem<scores_codes_kernel>((int)sizeof(Smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(NTHREADS);

@@ -323,10 +323,7 @@ kvq_status launch_step_small(const float *K, int64_t T, int64_t D, const float *
     const SmallLayout L = small_layout(w, G, D);
     const size_t smem = ((size_t)4 * SS_ROWS * SS_MAXQ + (size_t)SS_MAXQ * (SS_MAXD + 1) + SS_ROWS * SS_MAXD) * 8 +
                         (size_t)2 * SS_MAXD * 4;
-    static std::once_flag once;
-    std::call_once(once, [&] {
-        cudaFuncSetAttribute(step_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    });
+    ensure_max_smem<step_small_kernel>((int)smem);
     int Di = (int)D, nqi = (int)nq;
     const float *Qp = nq ? Q : nullptr;
     void *args[] = {(void *)&K, (void *)&T, (void *)&Di, (void *)&Qp, (void *)&nqi, (void *)&scales, (void *)&Kq,
